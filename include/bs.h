@@ -1,0 +1,268 @@
+/*
+ * bs.h — C ABI of libbs.so: batched point lookups over a densely packed sorted
+ * key array on NVIDIA B200 (sm_100a).  Method: Henneberg & Schuhknecht,
+ * "All You Need Is Binary Search! A Practical View on Lightweight Database
+ * Indexing on GPUs" (arXiv 2506.01576).  "P:n" below = PAPER.md line n.
+ *
+ * RESULT CONTRACT (every variant, every knob):
+ *   out[i] = lb(q_i)             if a[lb] == q_i           (hit: the rowID)
+ *          = lb(q_i) | MISS_BIT  otherwise                 (miss)
+ *   lb(q)  = #{ j : a[j] < q }  in [0, n], unsigned compares, a ascending,
+ *            duplicates allowed -> first occurrence.
+ *   MISS_BIT = 1 << 63 for 8-byte outputs, 1 << 31 for 4-byte outputs.
+ *
+ * MEMORY: unless stated otherwise pointers are CUDA DEVICE pointers on the
+ * current device.  Streams are cudaStream_t passed as void* (NULL = legacy
+ * default stream).  No torch / C++ types cross this boundary.
+ *
+ * ERRORS: every int-returning call returns a bs_status.  Nothing throws or
+ * aborts across the ABI.  bs_last_error() returns a thread-local message for
+ * the last non-OK status on the calling thread.  Asynchronous device faults
+ * of a bs_lookup surface at the caller's next synchronisation (or the next
+ * call that synchronises), as with any CUDA launch.
+ *
+ * THREADING: an index is immutable after bs_build; any number of bs_lookup
+ * calls on one index may run concurrently from many host threads / streams.
+ * bs_destroy must not race with lookups in flight (caller synchronises).
+ */
+#ifndef BS_H_
+#define BS_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    BS_OK = 0,
+    BS_ERR_INVALID = -1,      /* bad argument (see each call) */
+    BS_ERR_UNSUPPORTED = -2,  /* valid but not built into this library / index */
+    BS_ERR_OOM = -3,          /* device allocation failed */
+    BS_ERR_CUDA = -4,         /* a CUDA runtime call or launch failed */
+    BS_ERR_NCCL = -5,         /* an NCCL call failed (multi-GPU entry points) */
+    BS_ERR_NOT_SORTED = -6    /* input_sorted = 1 but keys are not ascending */
+} bs_status;
+
+typedef enum {
+    BS_VARIANT_NAIVE = 0,  /* Listing 1: one thread per lookup, dynamic grid    */
+    BS_VARIANT_OPT = 1,    /* §4: scheduling + pinning + reordering ("BS opt")  */
+    BS_VARIANT_KARY = 2    /* §5: warp-cooperative K-ary search ("KS")         */
+} bs_variant;
+
+typedef enum {
+    BS_SCHED_DYNAMIC = 0,  /* hardware block scheduler, one tile per CTA     */
+    BS_SCHED_STATIC = 1    /* persistent grid = SMs x ctas_per_sm, strided tiles   */
+} bs_schedule;
+
+typedef enum {
+    BS_REORDER_NONE = 0,
+    BS_REORDER_LOOKUP = 1, /* §4.3 "lookup-reordering": block-local sort, direct stores */
+    BS_REORDER_FULL = 2    /* §4.3 "full-reordering": + inverse permutation before a coalesced
+                              store (Listing 2 l.35-39)                                 */
+} bs_reorder;
+
+/* Build-time structure + default launch configuration.
+ * Fill with bs_layout_default() and override fields; struct_size guards ABI. */
+typedef struct {
+    uint32_t struct_size;   /* = sizeof(bs_layout)                                          */
+    uint32_t key_bytes;     /* 4 (u32) or 8 (u64); unsigned ordering                 */
+    uint32_t out_bytes;     /* 8, or 4 (requires n < 2^31)                                  */
+    uint32_t input_sorted;  /* 1: keys already ascending (validated on device);
+                               0: the library sorts a copy (unsigned radix sort)            */
+    uint32_t variant;       /* bs_variant used by bs_lookup                                 */
+    uint32_t schedule;      /* bs_schedule                                                  */
+    uint32_t threads;       /* threads per CTA (NBTHREAD); 0 = tuned default         */
+    uint32_t nreg;          /* lookups per thread (NREG, Listing 2 l.6) for OPT, interleaved
+                               lookup waves per warp for KARY; 0 = tuned default           */
+    uint32_t pin_bytes;     /* OPT: shared-memory budget for the pinned top search levels
+                               (§4.2); KARY: budget for the top separator levels
+                               kept in shared memory (§5.1); 0 = no pinning;
+                               0xFFFFFFFF = largest that fits                              */
+    uint32_t pin_partial;   /* OPT: 1 = "full-pinning" (partial step M+1), 0 = "steps-pinning" */
+    uint32_t reorder;       /* bs_reorder (OPT only)                                        */
+    uint32_t k;             /* KARY fan-out K, 2..33 (P:213, P:223 best K = 17)             */
+    uint32_t leaf_chunk;    /* KARY leaf chunk C in keys, power of two 1..256       */
+    uint32_t ctas_per_sm;   /* STATIC schedule: resident CTAs per SM; 0 = auto              */
+    uint32_t cache_hints;   /* bitmask BS_HINT_*; 0 = plain loads/stores                    */
+    uint32_t reserved[7];   /* must be 0                                                    */
+} bs_layout;
+
+/* cache_hints bits (B200 L2 eviction-priority hints; not in the paper) */
+#define BS_HINT_STREAM_EVICT_FIRST 1u  /* query loads / result stores: L2 evict_first    */
+#define BS_HINT_LEAF_EVICT_FIRST 2u    /* deepest probes / K-ary leaves: L2 evict_first  */
+
+/* Per-call launch override (bs_lookup_ex).  Only launch knobs; the structure
+ * built by bs_build (pinned table size, K, C) is fixed.  Field meaning as in
+ * bs_layout; 0 in threads/nreg/ctas_per_sm means "index default".           */
+typedef struct {
+    uint32_t struct_size;   /* = sizeof(bs_launch) */
+    uint32_t variant;
+    uint32_t schedule;
+    uint32_t threads;
+    uint32_t nreg;
+    uint32_t reorder;
+    uint32_t pin_partial;
+    uint32_t ctas_per_sm;
+    uint32_t cache_hints;
+    uint32_t use_pinned;    /* 1: use the pinned table / shared separator levels (if built) */
+    uint32_t reserved[6];
+} bs_launch;
+
+typedef struct {
+    uint32_t struct_size;        /* = sizeof(bs_info) */
+    uint32_t key_bytes, out_bytes;
+    uint64_t n;
+    uint64_t footprint_bytes;    /* all device memory owned by the index (Fig. 12) */
+    uint64_t array_bytes;        /* n * key_bytes                                         */
+    uint64_t pinned_entries;     /* level-major pinned table entries (OPT)                */
+    uint32_t pinned_levels;      /* M: complete levels pinned (§4.2)                      */
+    uint32_t pinned_partial;     /* entries of level M kept (full-pinning)         */
+    uint32_t search_levels;      /* total binary-search steps = floor(log2(n-1)) + 1      */
+    uint32_t kary_levels;        /* internal K-ary levels                                 */
+    uint32_t k, leaf_chunk, node_slots;
+    uint32_t kary_smem_levels;   /* top K-ary levels staged in shared memory              */
+    uint64_t separator_slots;    /* K-ary slots incl. padding (node_slots per node)       */
+    uint64_t separator_bytes;
+    double build_ms;             /* device time of bs_build (Fig. 13)               */
+    uint32_t sm_count;
+    uint32_t smem_per_cta_opt;   /* dynamic shared memory of the OPT kernel (bytes)       */
+    uint32_t smem_per_cta_kary;
+    uint32_t reserved[5];
+} bs_info;
+
+/* Debug exports (layout-fidelity tests) for bs_export(). */
+#define BS_EXPORT_SORTED 0   /* the sorted key array (n keys)                          */
+#define BS_EXPORT_PINNED 1   /* the level-major pinned table (pinned_entries keys)     */
+#define BS_EXPORT_KARY 2     /* K-ary separator slots, levels top-first (separator_slots) */
+
+/* Fills *l with defaults for u64 keys/outputs, K-ary K = 17 / C = 16, largest
+ * pin budget, static schedule.  BS_ERR_INVALID if l is NULL. */
+int bs_layout_default(bs_layout* l);
+
+/* Fills *l with the per-call defaults stored in idx. */
+int bs_launch_default(const void* idx, bs_launch* l);
+
+/*
+ * Builds an immutable index over n keys ("sorted input array of size n",
+ * P:119 pinned entries, P:213 K-ary separators, built bottom-up).
+ *   keys     device OR host pointer to n keys of layout->key_bytes each; the
+ *            library copies (and if input_sorted = 0 sorts) them into
+ *            library-owned device memory; the caller's buffer is untouched.
+ *   n        >= 1 (P:65 needs n-1 >= 0); out_bytes = 4 requires n < 2^31.
+ *   layout   see bs_layout; NULL = bs_layout_default().
+ *   out_idx  receives the index; NULL on error.
+ * Synchronous: returns when the index is ready.  Always builds the pinned
+ * table for OPT and the separator levels for KARY; the NAIVE variant needs
+ * neither.  Errors: BS_ERR_INVALID (NULL pointers, n == 0, bad widths, K not
+ * in [2,33], C not a power of two in [1,256], nonzero reserved fields),
+ * BS_ERR_NOT_SORTED, BS_ERR_OOM, BS_ERR_CUDA.
+ */
+int bs_build(const void* keys, uint64_t n, const bs_layout* layout, void** out_idx);
+
+/*
+ * Looks up m queries ("probes ... keys"; §4.4 Listing 2).
+ *   idx      from bs_build.
+ *   queries  device pointer, m keys of key_bytes (any alignment of the element
+ *            type).
+ *   m        0 is allowed (no launch, BS_OK).
+ *   out      device pointer, m words of out_bytes; must not overlap queries.
+ *   stream   cudaStream_t (void*); the call is stream-ordered and
+ *            asynchronous: no allocation, no host synchronisation.
+ * Errors: BS_ERR_INVALID (NULL idx / pointers with m > 0, overlap),
+ * BS_ERR_CUDA (launch failure).
+ */
+int bs_lookup(const void* idx, const void* queries, uint64_t m, void* out, void* stream);
+
+/* bs_lookup with per-call launch knobs (variant, schedule, threads, nreg,
+ * reorder, pinning use).  BS_ERR_UNSUPPORTED if the requested variant's
+ * structure was not built or the knob combination is not compiled in. */
+int bs_lookup_ex(const void* idx, const void* queries, uint64_t m, void* out, void* stream,
+                 const bs_launch* launch);
+
+/*
+ * End-to-end lookup from HOST memory: copies queries host->device, runs the
+ * index's default lookup, copies results device->host, in pipelined chunks
+ * on internal streams (copy of chunk i+1 overlaps lookup of chunk i and the
+ * copy-back of chunk i-1).
+ *   host_queries / host_out  host pointers (pinned memory gives full PCIe
+ *            bandwidth; pageable memory is staged through internal pinned
+ *            buffers).
+ *   stream   the call is ordered after prior work on `stream` and returns
+ *            when host_out is complete (synchronous).
+ * Allocates its staging buffers on first use per index (then reuses them;
+ * serialised by an internal mutex).  Errors as bs_lookup, plus BS_ERR_OOM.
+ */
+int bs_lookup_host(const void* idx, const void* host_queries, uint64_t m, void* host_out,
+                   void* stream);
+
+/* Frees everything the index owns.  NULL-safe.  No lookups may be in flight. */
+void bs_destroy(void* idx);
+
+/* Thread-local message for the last non-OK status ("" if none). */
+const char* bs_last_error(void);
+
+/* Sizes and structure of an index (Fig. 12 footprint, Fig. 13 build time). */
+int bs_index_info(const void* idx, bs_info* info);
+
+/* Copies one internal structure (BS_EXPORT_*) to HOST memory dst of `cap`
+ * bytes; *written = bytes copied.  Synchronous.  Test/debug use only.
+ * BS_ERR_INVALID if cap is too small, BS_ERR_UNSUPPORTED if not built. */
+int bs_export(const void* idx, int what, void* dst, uint64_t cap, uint64_t* written);
+
+/* Library version / build string (arch, commit-independent). */
+const char* bs_version(void);
+
+/* ------------------------------------------------------------------------
+ * Multi-GPU (one process per GPU; BASELINE.json configs 4-5, not in the
+ * paper).  REPLICATED: every rank builds the full index; queries are sharded
+ * by the caller; no collective on the lookup path.  PARTITIONED: rank r holds
+ * the contiguous rank range [base_r, base_r + n_r) of the global sorted
+ * array; bs_lookup_dist routes each query to the first shard whose maximum
+ * is >= q (else the last shard), looks it up there and returns the GLOBAL
+ * result (base + local lb, miss bit kept), in the caller's query order.
+ * ---------------------------------------------------------------------- */
+
+#define BS_DIST_REPLICATED 0
+#define BS_DIST_PARTITIONED 1
+
+/* Size of the NCCL unique id blob (bytes). */
+#define BS_DIST_UID_BYTES 128
+
+/* Rank 0 fills uid (BS_DIST_UID_BYTES host bytes); the caller broadcasts it
+ * (e.g. over torch.distributed's store) before every rank calls bs_dist_init. */
+int bs_dist_get_uid(void* uid);
+
+/* Creates the NCCL communicator for (rank, world) on the current device.
+ * Collective across ranks.  out_comm receives an opaque handle. */
+int bs_dist_init(const void* uid, int rank, int world, void** out_comm);
+
+/*
+ * Collective: builds this rank's index over its local, ascending keys
+ * (device pointer, n_local >= 1) and exchanges shard metadata (maxima and
+ * sizes) with ncclAllGather.  mode = BS_DIST_REPLICATED or
+ * BS_DIST_PARTITIONED.  max_m_local bounds m_local of later lookups (sizes
+ * the exchange buffers, allocated here).  Shards must be globally ordered by
+ * rank (max of rank r <= min of rank r+1) in PARTITIONED mode, checked.
+ */
+int bs_build_dist(void* comm, const void* local_keys, uint64_t n_local, int mode,
+                  const bs_layout* layout, uint64_t max_m_local, void** out_idx);
+
+/*
+ * Collective in PARTITIONED mode (every rank must call, m_local may be 0):
+ * route (k_route) -> count exchange -> query all-to-all (grouped
+ * ncclSend/ncclRecv) -> local lookup -> result all-to-all -> unroute.
+ * REPLICATED mode: a plain local bs_lookup, no communication.
+ * out_local receives global results (out_bytes must be 8 in PARTITIONED).
+ */
+int bs_lookup_dist(const void* idx, const void* local_queries, uint64_t m_local, void* out_local,
+                   void* stream);
+
+/* Destroys the communicator (after all dist indexes using it). NULL-safe. */
+void bs_dist_destroy(void* comm);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BS_H_ */

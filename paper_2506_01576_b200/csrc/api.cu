@@ -1,0 +1,391 @@
+// api.cu — the C ABI of libbs.so (include/bs.h): validation, index ownership,
+// build orchestration and variant dispatch.  Host code only; the kernels live
+// in naive.cu / opt.cu / kary.cu / build.cu.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "bs.h"
+#include "index.h"
+
+namespace bs {
+
+static thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+int fail_cuda(cudaError_t e, const char* what) {
+    cudaGetLastError();  // clear sticky-free errors
+    return fail(e == cudaErrorMemoryAllocation ? BS_ERR_OOM : BS_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+static bool reserved_zero(const uint32_t* r, int cnt) {
+    for (int i = 0; i < cnt; ++i)
+        if (r[i]) return false;
+    return true;
+}
+
+static bool is_pow2(uint64_t x) { return x && !(x & (x - 1)); }
+
+static uint32_t pow2_at_least(uint32_t x) {
+    uint32_t w = 1;
+    while (w < x) w <<= 1;
+    return w;
+}
+
+static void free_index(Index* ix) {
+    if (!ix) return;
+    if (ix->d_keys) cudaFree(ix->d_keys);
+    if (ix->d_tab) cudaFree(ix->d_tab);
+    if (ix->d_sep) cudaFree(ix->d_sep);
+    destroy_host_ctx(ix);
+    destroy_dist_state(ix);
+    delete ix;
+}
+
+// Offset-search level structure (DESIGN.md §"Pinned table").
+static void compute_levels(Index* ix) {
+    const uint64_t n = ix->n;
+    ix->s0 = (n >= 2) ? lpow2(n - 1) : 0;
+    ix->levels = 0;
+    if (n < 2) return;
+    uint32_t L = 0;
+    for (uint64_t s = ix->s0; s > 0; s >>= 1) ++L;
+    ix->levels = L;
+    uint64_t acc = 0;
+    for (uint32_t d = 0; d < L; ++d) {
+        const uint64_t sd = ix->s0 >> d;
+        const uint64_t F = (n - 1) / sd;
+        ix->valid_all[d] = (F + 1) / 2;      // k < valid_d  <=>  (2k+1) s_d <= n-1
+        ix->base_all[d] = acc;
+        acc += ix->valid_all[d];
+    }
+    ix->base_all[L] = acc;                   // == n-1
+}
+
+// Choose D / P for a table prefix of at most `entries` entries.
+void table_prefix(const Index* ix, uint64_t entries, bool partial, uint32_t* D, uint32_t* P) {
+    uint32_t d = 0;
+    while (d < ix->levels && ix->base_all[d + 1] <= entries) ++d;
+    uint64_t p = 0;
+    if (partial && d < ix->levels) {
+        p = entries - ix->base_all[d];
+        if (p > ix->valid_all[d]) p = ix->valid_all[d];
+    }
+    *D = d;
+    *P = (uint32_t)p;
+}
+
+static int build_kary_layout(Index* ix, cudaStream_t st) {
+    const uint64_t n = ix->n;
+    const uint32_t K = ix->kK, C = ix->kC, W = ix->kW;
+    // bottom-up node counts, then reverse to top-first
+    uint64_t counts[kMaxKaryLevels + 2];
+    uint32_t L = 0;
+    uint64_t c = (n + C - 1) / C;           // leaf chunks
+    const uint64_t chunks = c;
+    while (c > 1) {
+        if (L >= (uint32_t)kMaxKaryLevels) return fail(BS_ERR_INVALID, "K-ary tree deeper than %d levels", kMaxKaryLevels);
+        c = (c + K - 1) / K;
+        counts[L++] = c;
+    }
+    ix->kL = L;
+    const uint32_t kb = ix->kb;
+    const uint64_t align_slots = (W * kb >= 128) ? W : (128 / kb);   // level starts 128-B aligned
+    uint64_t slot = 0;
+    for (uint32_t l = 0; l < L; ++l) {
+        const uint64_t nodes = counts[L - 1 - l];
+        ix->k_nodes[l] = nodes;
+        ix->k_base[l] = slot;
+        slot += nodes * W;
+        slot = (slot + align_slots - 1) / align_slots * align_slots;
+    }
+    for (uint32_t l = 0; l < L; ++l) ix->k_next[l] = (l + 1 < L) ? ix->k_nodes[l + 1] : chunks;
+    ix->sep_slots = slot;
+    if (chunks > 0xFFFFFFFFull) return fail(BS_ERR_INVALID, "n / leaf_chunk must be < 2^32");
+    if (L == 0) return BS_OK;
+    const size_t bytes = slot * kb + 16;
+    cudaError_t e = cudaMalloc(&ix->d_sep, bytes);
+    if (e != cudaSuccess) return fail_cuda(e, "cudaMalloc(separators)");
+    e = cudaMemsetAsync(ix->d_sep, 0xFF, bytes, st);
+    if (e != cudaSuccess) return fail_cuda(e, "memset(separators)");
+    e = build_kary_levels(kb, ix->d_keys, n, K, C, W, L, ix->k_base, ix->k_nodes, ix->d_sep, slot, st);
+    if (e != cudaSuccess) return fail_cuda(e, "build_kary_levels");
+    return BS_OK;
+}
+
+}  // namespace bs
+
+using namespace bs;
+
+extern "C" {
+
+const char* bs_last_error(void) { return g_err.c_str(); }
+
+const char* bs_version(void) {
+    return "libbs 0.1 (sm_100a; naive / opt / kary; arXiv 2506.01576)";
+}
+
+int bs_layout_default(bs_layout* l) {
+    if (!l) return fail(BS_ERR_INVALID, "bs_layout_default: NULL");
+    memset(l, 0, sizeof *l);
+    l->struct_size = sizeof(bs_layout);
+    l->key_bytes = 8;
+    l->out_bytes = 8;
+    l->input_sorted = 1;
+    l->variant = BS_VARIANT_KARY;
+    l->schedule = BS_SCHED_STATIC;
+    l->threads = 0;
+    l->nreg = 0;
+    l->pin_bytes = 0xFFFFFFFFu;
+    l->pin_partial = 1;
+    l->reorder = BS_REORDER_NONE;
+    l->k = 17;
+    l->leaf_chunk = 16;
+    l->ctas_per_sm = 0;
+    l->cache_hints = BS_HINT_STREAM_EVICT_FIRST | BS_HINT_LEAF_EVICT_FIRST;
+    return BS_OK;
+}
+
+int bs_build(const void* keys, uint64_t n, const bs_layout* layout_in, void** out_idx) {
+    if (!out_idx) return fail(BS_ERR_INVALID, "bs_build: out_idx is NULL");
+    *out_idx = nullptr;
+    bs_layout lay;
+    if (layout_in) {
+        if (layout_in->struct_size != sizeof(bs_layout))
+            return fail(BS_ERR_INVALID, "bs_build: layout.struct_size %u != %zu", layout_in->struct_size, sizeof(bs_layout));
+        lay = *layout_in;
+    } else {
+        bs_layout_default(&lay);
+    }
+    if (!keys) return fail(BS_ERR_INVALID, "bs_build: keys is NULL");
+    if (n == 0) return fail(BS_ERR_INVALID, "bs_build: n == 0 (the offset search needs n >= 1, P:65)");
+    if (lay.key_bytes != 4 && lay.key_bytes != 8) return fail(BS_ERR_INVALID, "key_bytes must be 4 or 8");
+    if (lay.out_bytes != 4 && lay.out_bytes != 8) return fail(BS_ERR_INVALID, "out_bytes must be 4 or 8");
+    if (lay.out_bytes == 4 && n >= (1ull << 31)) return fail(BS_ERR_INVALID, "out_bytes = 4 requires n < 2^31");
+    if (lay.variant > BS_VARIANT_KARY) return fail(BS_ERR_INVALID, "unknown variant %u", lay.variant);
+    if (lay.schedule > BS_SCHED_STATIC) return fail(BS_ERR_INVALID, "unknown schedule %u", lay.schedule);
+    if (lay.reorder > BS_REORDER_FULL) return fail(BS_ERR_INVALID, "unknown reorder %u", lay.reorder);
+    if (lay.k < 2 || lay.k > 33) return fail(BS_ERR_INVALID, "K must be in [2, 33]");
+    if (!is_pow2(lay.leaf_chunk) || lay.leaf_chunk > 256) return fail(BS_ERR_INVALID, "leaf_chunk must be a power of two <= 256");
+    if (!reserved_zero(lay.reserved, 7)) return fail(BS_ERR_INVALID, "layout.reserved must be zero");
+    if (lay.threads > 1024 || lay.threads % 32) return fail(BS_ERR_INVALID, "threads must be a multiple of 32 <= 1024");
+
+    Index* ix = new Index();
+    ix->layout = lay;
+    ix->n = n;
+    ix->kb = lay.key_bytes;
+    ix->ob = lay.out_bytes;
+    int rc = BS_OK;
+    cudaError_t e;
+    cudaStream_t st = nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    int* d_flag = nullptr;
+    const size_t abytes = n * ix->kb;
+
+    e = cudaGetDevice(&ix->device);
+    if (e != cudaSuccess) { rc = fail_cuda(e, "cudaGetDevice"); goto done; }
+    {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, ix->device); ix->sm_count = v;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, ix->device); ix->smem_optin = v;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerMultiprocessor, ix->device); ix->smem_per_sm = v;
+        cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, ix->device); ix->l2_bytes = v;
+    }
+    e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    if (e != cudaSuccess) { rc = fail_cuda(e, "cudaStreamCreate"); goto done; }
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, st);
+
+    // ---- the sorted array ----
+    e = cudaMalloc(&ix->d_keys, abytes + 16);
+    if (e != cudaSuccess) { rc = fail_cuda(e, "cudaMalloc(keys)"); goto done; }
+    {
+        cudaPointerAttributes pa;
+        const bool dev = cudaPointerGetAttributes(&pa, keys) == cudaSuccess &&
+                         (pa.type == cudaMemoryTypeDevice || pa.type == cudaMemoryTypeManaged);
+        cudaGetLastError();
+        if (lay.input_sorted) {
+            e = cudaMemcpyAsync(ix->d_keys, keys, abytes, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st);
+            if (e != cudaSuccess) { rc = fail_cuda(e, "copy keys"); goto done; }
+            e = cudaMallocAsync((void**)&d_flag, sizeof(int), st);
+            if (e != cudaSuccess) { rc = fail_cuda(e, "cudaMalloc(flag)"); goto done; }
+            cudaMemsetAsync(d_flag, 0, sizeof(int), st);
+            e = build_check_sorted(ix->kb, ix->d_keys, n, d_flag, st);
+            if (e != cudaSuccess) { rc = fail_cuda(e, "check_sorted"); goto done; }
+            int flag = 0;
+            cudaMemcpyAsync(&flag, d_flag, sizeof(int), cudaMemcpyDeviceToHost, st);
+            e = cudaStreamSynchronize(st);
+            if (e != cudaSuccess) { rc = fail_cuda(e, "check_sorted sync"); goto done; }
+            if (flag) { rc = fail(BS_ERR_NOT_SORTED, "bs_build: input_sorted = 1 but keys are not ascending"); goto done; }
+        } else {
+            void* tmp = nullptr;
+            e = cudaMallocAsync(&tmp, abytes, st);
+            if (e != cudaSuccess) { rc = fail_cuda(e, "cudaMalloc(sort tmp)"); goto done; }
+            e = cudaMemcpyAsync(tmp, keys, abytes, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st);
+            if (e == cudaSuccess) e = build_sort_keys(ix->kb, tmp, ix->d_keys, n, st);
+            cudaFreeAsync(tmp, st);
+            if (e != cudaSuccess) { rc = fail_cuda(e, "radix sort"); goto done; }
+        }
+        e = cudaMemcpyAsync(&ix->a_last, (const char*)ix->d_keys + (n - 1) * ix->kb, ix->kb, cudaMemcpyDeviceToHost, st);
+        if (e != cudaSuccess) { rc = fail_cuda(e, "read a[n-1]"); goto done; }
+        e = cudaMemcpyAsync(&ix->a_first, ix->d_keys, ix->kb, cudaMemcpyDeviceToHost, st);
+        if (e != cudaSuccess) { rc = fail_cuda(e, "read a[0]"); goto done; }
+    }
+
+    // ---- level-major pinned table (§4.2) ----
+    compute_levels(ix);
+    {
+        uint64_t cap = (uint64_t)ix->smem_optin / ix->kb;
+        if (lay.pin_bytes != 0xFFFFFFFFu) cap = lay.pin_bytes / ix->kb;
+        uint64_t entries = (n >= 2) ? (n - 1) : 0;
+        if (entries > cap) entries = cap;
+        ix->tab_entries = entries;
+        if (entries) {
+            e = cudaMalloc(&ix->d_tab, entries * ix->kb + 16);
+            if (e != cudaSuccess) { rc = fail_cuda(e, "cudaMalloc(table)"); goto done; }
+            uint32_t bases[kMaxLevels + 1];
+            for (uint32_t d = 0; d <= ix->levels; ++d) bases[d] = (uint32_t)(ix->base_all[d] < 0xFFFFFFFFull ? ix->base_all[d] : 0xFFFFFFFFu);
+            e = build_pinned_table(ix->kb, ix->d_keys, n, ix->s0, ix->levels, bases, ix->d_tab, entries, st);
+            if (e != cudaSuccess) { rc = fail_cuda(e, "build_pinned_table"); goto done; }
+        }
+    }
+
+    // ---- K-ary separator levels (§5) ----
+    ix->kK = lay.k;
+    ix->kC = lay.leaf_chunk;
+    ix->kW = pow2_at_least(lay.k - 1 < 2 ? 2 : lay.k - 1);
+    if (ix->kW > 32) { rc = fail(BS_ERR_INVALID, "K - 1 must be <= 32"); goto done; }
+    if (lay.variant == BS_VARIANT_KARY) {
+        rc = build_kary_layout(ix, st);
+        if (rc != BS_OK) goto done;
+        ix->kary_built = true;
+    }
+
+    cudaEventRecord(e1, st);
+    e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) { rc = fail_cuda(e, "bs_build sync"); goto done; }
+    {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        ix->build_ms = ms;
+    }
+
+done:
+    if (d_flag) { cudaFreeAsync(d_flag, st); }
+    if (st) { cudaStreamSynchronize(st); cudaStreamDestroy(st); }
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+    if (rc != BS_OK) { free_index(ix); return rc; }
+    *out_idx = ix;
+    return BS_OK;
+}
+
+void bs_destroy(void* idx) { free_index((Index*)idx); }
+
+int bs_launch_default(const void* idx, bs_launch* l) {
+    if (!idx || !l) return fail(BS_ERR_INVALID, "bs_launch_default: NULL");
+    const Index* ix = (const Index*)idx;
+    memset(l, 0, sizeof *l);
+    l->struct_size = sizeof(bs_launch);
+    l->variant = ix->layout.variant;
+    l->schedule = ix->layout.schedule;
+    l->threads = ix->layout.threads;
+    l->nreg = ix->layout.nreg;
+    l->reorder = ix->layout.reorder;
+    l->pin_partial = ix->layout.pin_partial;
+    l->ctas_per_sm = ix->layout.ctas_per_sm;
+    l->cache_hints = ix->layout.cache_hints;
+    l->use_pinned = ix->layout.pin_bytes != 0;
+    return BS_OK;
+}
+
+int bs_lookup_ex(const void* idx, const void* queries, uint64_t m, void* out, void* stream, const bs_launch* launch) {
+    if (!idx) return fail(BS_ERR_INVALID, "bs_lookup: idx is NULL");
+    const Index* ix = (const Index*)idx;
+    bs_launch L;
+    if (launch) {
+        if (launch->struct_size != sizeof(bs_launch)) return fail(BS_ERR_INVALID, "bs_launch.struct_size mismatch");
+        L = *launch;
+    } else {
+        bs_launch_default(idx, &L);
+    }
+    if (m == 0) return BS_OK;
+    if (!queries || !out) return fail(BS_ERR_INVALID, "bs_lookup: NULL queries/out with m > 0");
+    const uintptr_t q0 = (uintptr_t)queries, q1 = q0 + m * ix->kb;
+    const uintptr_t o0 = (uintptr_t)out, o1 = o0 + m * ix->ob;
+    if (q0 < o1 && o0 < q1) return fail(BS_ERR_INVALID, "bs_lookup: out overlaps queries");
+    if (q0 % ix->kb || o0 % ix->ob) return fail(BS_ERR_INVALID, "bs_lookup: misaligned queries/out");
+    return dispatch_lookup(ix, queries, m, out, (cudaStream_t)stream, L);
+}
+
+int bs_lookup(const void* idx, const void* queries, uint64_t m, void* out, void* stream) {
+    return bs_lookup_ex(idx, queries, m, out, stream, nullptr);
+}
+
+int bs_index_info(const void* idx, bs_info* info) {
+    if (!idx || !info) return fail(BS_ERR_INVALID, "bs_index_info: NULL");
+    const Index* ix = (const Index*)idx;
+    memset(info, 0, sizeof *info);
+    info->struct_size = sizeof(bs_info);
+    info->key_bytes = ix->kb;
+    info->out_bytes = ix->ob;
+    info->n = ix->n;
+    info->array_bytes = ix->n * ix->kb;
+    info->pinned_entries = ix->tab_entries;
+    uint32_t D = 0, P = 0;
+    uint64_t budget = ix->tab_entries;
+    table_prefix(ix, budget, ix->layout.pin_partial != 0, &D, &P);
+    info->pinned_levels = D;
+    info->pinned_partial = P;
+    info->search_levels = ix->levels;
+    info->kary_levels = ix->kL;
+    info->k = ix->kK;
+    info->leaf_chunk = ix->kC;
+    info->node_slots = ix->kW;
+    info->separator_slots = ix->kary_built ? ix->sep_slots : 0;
+    info->separator_bytes = info->separator_slots * ix->kb;
+    info->kary_smem_levels = ix->kary_built ? kary_smem_levels(ix, nullptr) : 0;
+    info->footprint_bytes = info->array_bytes + ix->tab_entries * ix->kb + info->separator_bytes;
+    info->build_ms = ix->build_ms;
+    info->sm_count = ix->sm_count;
+    info->smem_per_cta_opt = (uint32_t)ix->last_opt_smem;
+    info->smem_per_cta_kary = (uint32_t)ix->last_kary_smem;
+    return BS_OK;
+}
+
+int bs_export(const void* idx, int what, void* dst, uint64_t cap, uint64_t* written) {
+    if (!idx || !dst || !written) return fail(BS_ERR_INVALID, "bs_export: NULL");
+    const Index* ix = (const Index*)idx;
+    const void* src = nullptr;
+    uint64_t bytes = 0;
+    switch (what) {
+        case BS_EXPORT_SORTED: src = ix->d_keys; bytes = ix->n * ix->kb; break;
+        case BS_EXPORT_PINNED: src = ix->d_tab; bytes = ix->tab_entries * ix->kb; break;
+        case BS_EXPORT_KARY:
+            if (!ix->kary_built) return fail(BS_ERR_UNSUPPORTED, "bs_export: K-ary levels not built");
+            src = ix->d_sep; bytes = ix->sep_slots * ix->kb; break;
+        default: return fail(BS_ERR_INVALID, "bs_export: unknown structure %d", what);
+    }
+    if (cap < bytes) return fail(BS_ERR_INVALID, "bs_export: cap %llu < %llu bytes", (unsigned long long)cap, (unsigned long long)bytes);
+    *written = 0;
+    if (bytes) {
+        cudaError_t e = cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) return fail_cuda(e, "bs_export copy");
+    }
+    *written = bytes;
+    return BS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,137 @@
+// build.cu — index construction kernels (bs_build; not on the lookup path).
+//   * unsigned radix sort of a key copy (CUB DeviceRadixSort) when the caller's
+//     keys are not declared sorted;
+//   * sortedness check when they are;
+//   * level-major pinned table (§4.2): T[base_d + k] = a[n-1-(2k+1)(s0>>d)];
+//   * K-ary separator levels (§5): slot j of node m at level l (top-first)
+//     = a[min((mK+j+1)*span_l, n) - 1] if (mK+j)*span_l < n and j < K-1, else MAX,
+//     span_l = C * K^(L-1-l).
+#include <cub/device/device_radix_sort.cuh>
+
+#include "common.cuh"
+#include "params.h"
+
+namespace bs {
+
+template <class K>
+__global__ void k_check_sorted(const K* __restrict__ a, uint64_t n, int* flag) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i + 1 < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        if (a[i] > a[i + 1]) { atomicOr(flag, 1); return; }
+    }
+}
+
+struct LevelBases { uint32_t base[kMaxLevels + 1]; };
+
+template <class K>
+__global__ void k_build_table(const K* __restrict__ a, uint64_t n, uint64_t s0, uint32_t nlev,
+                              LevelBases lb, K* __restrict__ tab, uint64_t entries) {
+    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < entries;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t d = 0;
+        while (d + 1 < nlev && lb.base[d + 1] <= e) ++d;
+        const uint64_t k = e - lb.base[d];
+        const uint64_t pos = n - 1 - (2 * k + 1) * (s0 >> d);
+        tab[e] = a[pos];
+    }
+}
+
+struct KaryMeta {
+    uint64_t start[kMaxKaryLevels + 1];  // slot offset of level l (top-first, padded)
+    uint64_t end[kMaxKaryLevels];        // start[l] + nodes_l * W (slots past it are padding)
+    uint64_t span[kMaxKaryLevels];       // keys per child at level l
+};
+
+template <class K>
+__global__ void k_build_kary(const K* __restrict__ a, uint64_t n, uint32_t Kf, uint32_t W, uint32_t L,
+                             KaryMeta meta, K* __restrict__ sep, uint64_t slots) {
+    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < slots;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t l = 0;
+        while (l + 1 < L && meta.start[l + 1] <= e) ++l;
+        const uint64_t rel = e - meta.start[l];
+        const uint64_t node = rel / W, j = rel % W;
+        K v = KeyMax<K>::v;
+        if (e < meta.end[l] && j + 1 < Kf) {
+            const uint64_t child = node * Kf + j;
+            const uint64_t span = meta.span[l];
+            if (child * span < n) {
+                uint64_t end = (child + 1) * span;
+                if (end > n) end = n;
+                v = a[end - 1];
+            }
+        }
+        sep[e] = v;
+    }
+}
+
+static unsigned grid_for(uint64_t work, unsigned threads) {
+    uint64_t g = (work + threads - 1) / threads;
+    if (g > 148ull * 64) g = 148ull * 64;
+    if (g == 0) g = 1;
+    return (unsigned)g;
+}
+
+cudaError_t build_check_sorted(int kb, const void* a, uint64_t n, int* d_flag, cudaStream_t s) {
+    if (n < 2) return cudaSuccess;
+    if (kb == 8) k_check_sorted<uint64_t><<<grid_for(n, 256), 256, 0, s>>>((const uint64_t*)a, n, d_flag);
+    else k_check_sorted<uint32_t><<<grid_for(n, 256), 256, 0, s>>>((const uint32_t*)a, n, d_flag);
+    return cudaGetLastError();
+}
+
+cudaError_t build_pinned_table(int kb, const void* a, uint64_t n, uint64_t s0, uint32_t nlev,
+                               const uint32_t* base, void* tab, uint64_t entries, cudaStream_t s) {
+    if (entries == 0) return cudaSuccess;
+    LevelBases lb{};
+    for (uint32_t d = 0; d <= nlev && d <= (uint32_t)kMaxLevels; ++d) lb.base[d] = base[d];
+    if (kb == 8)
+        k_build_table<uint64_t><<<grid_for(entries, 256), 256, 0, s>>>((const uint64_t*)a, n, s0, nlev, lb,
+                                                                      (uint64_t*)tab, entries);
+    else
+        k_build_table<uint32_t><<<grid_for(entries, 256), 256, 0, s>>>((const uint32_t*)a, n, s0, nlev, lb,
+                                                                      (uint32_t*)tab, entries);
+    return cudaGetLastError();
+}
+
+cudaError_t build_kary_levels(int kb, const void* a, uint64_t n, uint32_t Kf, uint32_t C, uint32_t W,
+                              uint32_t L, const uint64_t* lvl_base, const uint64_t* lvl_nodes,
+                              void* sep, uint64_t slots, cudaStream_t s) {
+    if (slots == 0 || L == 0) return cudaSuccess;
+    KaryMeta meta{};
+    for (uint32_t l = 0; l < L; ++l) {
+        meta.start[l] = lvl_base[l];
+        meta.end[l] = lvl_base[l] + lvl_nodes[l] * W;   // slots up to start[l+1] are MAX padding
+        uint64_t span = C;
+        for (uint32_t t = l + 1; t < L; ++t) span *= Kf;   // bottom level (l = L-1) spans C
+        meta.span[l] = span;
+    }
+    meta.start[L] = slots;
+    if (kb == 8)
+        k_build_kary<uint64_t><<<grid_for(slots, 256), 256, 0, s>>>((const uint64_t*)a, n, Kf, W, L, meta,
+                                                                    (uint64_t*)sep, slots);
+    else
+        k_build_kary<uint32_t><<<grid_for(slots, 256), 256, 0, s>>>((const uint32_t*)a, n, Kf, W, L, meta,
+                                                                    (uint32_t*)sep, slots);
+    return cudaGetLastError();
+}
+
+cudaError_t build_sort_keys(int kb, const void* in, void* out, uint64_t n, cudaStream_t s) {
+    size_t tmp_bytes = 0;
+    cudaError_t e;
+    if (kb == 8)
+        e = cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, (const uint64_t*)in, (uint64_t*)out, (int64_t)n, 0, 64, s);
+    else
+        e = cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, (const uint32_t*)in, (uint32_t*)out, (int64_t)n, 0, 32, s);
+    if (e != cudaSuccess) return e;
+    void* tmp = nullptr;
+    e = cudaMallocAsync(&tmp, tmp_bytes, s);
+    if (e != cudaSuccess) return e;
+    if (kb == 8)
+        e = cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, (const uint64_t*)in, (uint64_t*)out, (int64_t)n, 0, 64, s);
+    else
+        e = cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, (const uint32_t*)in, (uint32_t*)out, (int64_t)n, 0, 32, s);
+    cudaFreeAsync(tmp, s);
+    return e;
+}
+
+}  // namespace bs

@@ -1,0 +1,67 @@
+// index.h — the index object behind the opaque bs_index handle (internal).
+#pragma once
+#include <cstdint>
+#include <mutex>
+
+#include <cuda_runtime.h>
+
+#include "bs.h"
+#include "common.cuh"
+#include "params.h"
+
+namespace bs {
+
+struct HostCtx;    // bs_lookup_host staging (host.cu)
+struct DistState;  // multi-GPU exchange state (dist.cu)
+
+struct Index {
+    bs_layout layout{};
+    int device = 0;
+    uint32_t kb = 8, ob = 8;
+    uint64_t n = 0;
+    void* d_keys = nullptr;          // sorted array, n keys (+16 B slack)
+    uint64_t a_last = 0, a_first = 0;  // a[n-1], a[0] (low kb bytes valid)
+
+    // offset-search level structure (all levels) and the level-major table prefix
+    uint64_t s0 = 0;
+    uint32_t levels = 0;
+    uint64_t valid_all[kMaxLevels + 1] = {};
+    uint64_t base_all[kMaxLevels + 1] = {};
+    void* d_tab = nullptr;
+    uint64_t tab_entries = 0;
+
+    // K-ary
+    bool kary_built = false;
+    void* d_sep = nullptr;
+    uint32_t kK = 17, kC = 16, kW = 16, kL = 0;
+    uint64_t k_base[kMaxKaryLevels] = {};
+    uint64_t k_nodes[kMaxKaryLevels] = {};
+    uint64_t k_next[kMaxKaryLevels] = {};
+    uint64_t sep_slots = 0;
+
+    // device
+    int sm_count = 148, smem_optin = 232448, smem_per_sm = 233472, l2_bytes = 0;
+    double build_ms = 0;
+    mutable uint64_t last_opt_smem = 0, last_kary_smem = 0;
+
+    // lazily created host-path context
+    std::mutex host_mu;
+    HostCtx* host = nullptr;
+
+    // multi-GPU
+    DistState* dist = nullptr;
+};
+
+int fail(int code, const char* fmt, ...);
+int fail_cuda(cudaError_t e, const char* what);
+void table_prefix(const Index* ix, uint64_t entries, bool partial, uint32_t* D, uint32_t* P);
+
+// lookup.cu
+int dispatch_lookup(const Index* ix, const void* q, uint64_t m, void* out, cudaStream_t s, const bs_launch& L);
+uint32_t kary_smem_levels(const Index* ix, uint32_t* bytes_out, uint64_t cap_bytes = 0);
+
+// host.cu / dist.cu
+void destroy_host_ctx(Index* ix);
+void destroy_dist_state(Index* ix);
+
+}  // namespace bs

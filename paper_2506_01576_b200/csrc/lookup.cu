@@ -1,0 +1,150 @@
+// lookup.cu — per-call variant dispatch: builds the kernel parameter blocks
+// from the index and the launch knobs, sizes shared memory, launches.
+#include <cstring>
+
+#include "index.h"
+
+namespace bs {
+
+static uint32_t round16(uint64_t b) { return (uint32_t)((b + 15) & ~15ull); }
+
+static uint32_t bitlen(uint64_t x) {
+    uint32_t b = 0;
+    while (x) { ++b; x >>= 1; }
+    return b;
+}
+
+// shared memory one CTA may use when `c` CTAs share an SM (1 KB per CTA is
+// reserved by the system on sm_100)
+static uint64_t smem_cap(const Index* ix, uint32_t c) {
+    if (c == 0) c = 1;
+    uint64_t per = (uint64_t)ix->smem_per_sm / c;
+    per = per > 1024 ? per - 1024 : 0;
+    if (per > (uint64_t)ix->smem_optin) per = ix->smem_optin;
+    return per & ~15ull;
+}
+
+uint32_t kary_smem_levels(const Index* ix, uint32_t* bytes_out, uint64_t cap_bytes) {
+    if (cap_bytes == 0) cap_bytes = smem_cap(ix, 1) - 16;
+    if (ix->layout.pin_bytes != 0xFFFFFFFFu && ix->layout.pin_bytes < cap_bytes) cap_bytes = ix->layout.pin_bytes;
+    uint32_t Ls = 0;
+    while (Ls < ix->kL) {
+        const uint64_t end = (Ls + 1 < ix->kL) ? ix->k_base[Ls + 1] : ix->sep_slots;
+        if (end * ix->kb > cap_bytes) break;
+        ++Ls;
+    }
+    if (bytes_out) *bytes_out = Ls ? round16((Ls < ix->kL ? ix->k_base[Ls] : ix->sep_slots) * ix->kb) : 0;
+    return Ls;
+}
+
+template <class K>
+static int run_opt(const Index* ix, const void* q, uint64_t m, void* out, cudaStream_t s, const bs_launch& L) {
+    OptParams<K> p;
+    memset(&p, 0, sizeof p);
+    p.a = (const K*)ix->d_keys;
+    p.n = ix->n;
+    p.a_last = (K)ix->a_last;
+    p.s0 = ix->s0;
+    p.levels = ix->levels;
+    p.tab = (const K*)ix->d_tab;
+    const uint32_t threads = L.threads ? L.threads : 256;
+    const uint32_t nreg = L.nreg ? L.nreg : 8;
+    if (threads % 32 || threads > 1024) return fail(BS_ERR_INVALID, "threads must be a multiple of 32 <= 1024");
+    const uint32_t extra = opt_smem_extra(ix->kb, ix->ob, threads, nreg, L.reorder);
+    const uint32_t cps = L.schedule == BS_SCHED_STATIC ? L.ctas_per_sm : 0;
+    const uint64_t cap = smem_cap(ix, cps ? cps : 1);
+    if (extra > cap) return fail(BS_ERR_UNSUPPORTED, "OPT: tile of %u x %u does not fit shared memory", threads, nreg);
+    uint64_t entries = 0;
+    if (L.use_pinned && ix->d_tab) {
+        uint64_t budget = cap - extra;
+        if (ix->layout.pin_bytes != 0xFFFFFFFFu && ix->layout.pin_bytes < budget) budget = ix->layout.pin_bytes;
+        entries = budget / ix->kb;
+        if (entries > ix->tab_entries) entries = ix->tab_entries;
+    }
+    uint32_t D = 0, P = 0;
+    table_prefix(ix, entries, L.pin_partial != 0, &D, &P);
+    if (D >= (uint32_t)kMaxLevels) D = kMaxLevels - 1;
+    p.D = D;
+    p.P = P;
+    for (uint32_t d = 0; d <= D && d < (uint32_t)kMaxLevels; ++d) {
+        p.valid[d] = (uint32_t)ix->valid_all[d];
+        p.base[d] = (uint32_t)ix->base_all[d];
+    }
+    const uint64_t used = ix->base_all[D] + P;
+    p.tab_bytes = used ? round16(used * ix->kb) : 0;
+    // global-phase steps whose levels cannot stay in (half of) L2 get evict_first
+    const uint64_t l2 = ix->l2_bytes ? (uint64_t)ix->l2_bytes : (126ull << 20);
+    uint64_t es = 1;
+    while (es < (32ull * ix->n) / (l2 / 2)) es <<= 1;
+    p.evict_step = es;
+    p.stream_hint = (L.cache_hints & BS_HINT_STREAM_EVICT_FIRST) ? 1 : 0;
+    p.leaf_hint = (L.cache_hints & BS_HINT_LEAF_EVICT_FIRST) ? 1 : 0;
+    p.kmin = (K)ix->a_first;
+    const uint64_t range = (uint64_t)((K)ix->a_last - (K)ix->a_first);
+    const uint32_t tb = bitlen(threads * nreg) - 1;
+    const uint32_t rb = bitlen(range);
+    p.shift = rb > tb ? rb - tb : 0;
+    const uint32_t smem = p.tab_bytes + extra;
+    ix->last_opt_smem = smem;
+    bool uns = false;
+    Grid g{L.schedule == BS_SCHED_STATIC ? 1u : 0u, L.ctas_per_sm, (uint32_t)ix->sm_count};
+    cudaError_t e = launch_opt(ix->kb, ix->ob, &p, q, m, out, threads, nreg, L.reorder, g, smem, s, &uns);
+    if (uns) return fail(BS_ERR_UNSUPPORTED, "OPT: threads=%u nreg=%u reorder=%u not supported", threads, nreg, L.reorder);
+    if (e != cudaSuccess) return fail_cuda(e, "OPT launch");
+    return BS_OK;
+}
+
+template <class K>
+static int run_kary(const Index* ix, const void* q, uint64_t m, void* out, cudaStream_t s, const bs_launch& L) {
+    if (!ix->kary_built) return fail(BS_ERR_UNSUPPORTED, "KARY: index built without K-ary levels (layout.variant != KARY)");
+    KaryParams<K> p;
+    memset(&p, 0, sizeof p);
+    p.a = (const K*)ix->d_keys;
+    p.n = ix->n;
+    p.sep = (const K*)ix->d_sep;
+    p.L = ix->kL;
+    p.K = ix->kK;
+    p.C = ix->kC;
+    for (uint32_t l = 0; l < ix->kL; ++l) {
+        p.lvl_base[l] = ix->k_base[l];
+        p.nodes_next[l] = (uint32_t)ix->k_next[l];
+    }
+    const uint32_t threads = L.threads ? L.threads : 512;
+    const uint32_t R = L.nreg ? L.nreg : 2;
+    const bool stat = L.schedule == BS_SCHED_STATIC;
+    uint32_t Ls = 0, sbytes = 0;
+    if (stat && L.use_pinned) {
+        const uint64_t cap = smem_cap(ix, L.ctas_per_sm ? L.ctas_per_sm : 1) - 16;
+        Ls = kary_smem_levels(ix, &sbytes, cap);
+    }
+    p.Ls = Ls;
+    p.smem_bytes = sbytes;
+    p.stream_hint = (L.cache_hints & BS_HINT_STREAM_EVICT_FIRST) ? 1 : 0;
+    p.leaf_hint = (L.cache_hints & BS_HINT_LEAF_EVICT_FIRST) ? 1 : 0;
+    const uint32_t smem = sbytes + 16;
+    ix->last_kary_smem = smem;
+    bool uns = false;
+    Grid g{stat ? 1u : 0u, L.ctas_per_sm, (uint32_t)ix->sm_count};
+    cudaError_t e = launch_kary(ix->kb, ix->ob, &p, q, m, out, threads, ix->kW, R, g, smem, s, &uns);
+    if (uns) return fail(BS_ERR_UNSUPPORTED, "KARY: threads=%u waves=%u W=%u not supported", threads, R, ix->kW);
+    if (e != cudaSuccess) return fail_cuda(e, "KARY launch");
+    return BS_OK;
+}
+
+int dispatch_lookup(const Index* ix, const void* q, uint64_t m, void* out, cudaStream_t s, const bs_launch& L) {
+    switch (L.variant) {
+        case BS_VARIANT_NAIVE: {
+            cudaError_t e = launch_naive(ix->kb, ix->ob, ix->d_keys, ix->n, q, m, out, L.threads, s);
+            if (e != cudaSuccess) return fail_cuda(e, "NAIVE launch");
+            return BS_OK;
+        }
+        case BS_VARIANT_OPT:
+            return ix->kb == 8 ? run_opt<uint64_t>(ix, q, m, out, s, L) : run_opt<uint32_t>(ix, q, m, out, s, L);
+        case BS_VARIANT_KARY:
+            return ix->kb == 8 ? run_kary<uint64_t>(ix, q, m, out, s, L) : run_kary<uint32_t>(ix, q, m, out, s, L);
+        default:
+            return fail(BS_ERR_INVALID, "unknown variant %u", L.variant);
+    }
+}
+
+}  // namespace bs

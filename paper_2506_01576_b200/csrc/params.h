@@ -1,0 +1,82 @@
+// params.h — kernel parameter blocks and launcher declarations (internal to libbs.so).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace bs {
+
+constexpr int kMaxLevels = 48;      // binary-search levels (n < 2^48)
+constexpr int kMaxKaryLevels = 40;  // K-ary internal levels
+
+// Level-major pinned table (DESIGN.md §"Pinned table"; §4.2).
+// Level d of the offset search probes positions n-1-(2k+1)*s_d, s_d = s0 >> d,
+// s0 = LPOW2(n-1), for k < valid_d; the table stores T[base_d + k] = a[that].
+template <class K>
+struct OptParams {
+    const K* a;           // sorted array (device)
+    uint64_t n;
+    K a_last;             // a[n-1] (footnote 1: "first entry of the search path")
+    uint64_t s0;          // LPOW2(n-1) (first effective step), 0 if n == 1
+    uint32_t levels;      // total offset-search levels Dtot = log2(s0)+1 (0 if n == 1)
+    const K* tab;         // level-major table (device), 16-B padded
+    uint32_t tab_bytes;   // bytes staged into shared memory (0 = no pinning)
+    uint32_t D;           // complete levels staged
+    uint32_t P;           // entries of level D staged (full-pinning), 0 = steps-pinning
+    uint32_t valid[kMaxLevels];
+    uint32_t base[kMaxLevels];
+    uint64_t evict_step;  // global-phase steps < evict_step use the evict_first hint
+    uint32_t stream_hint; // 1: queries/results with L2 evict_first
+    uint32_t leaf_hint;   // 1: deep probes with L2 evict_first
+    // block-local reordering (§4.3): bucket = min((q - kmin) >> shift, nbuckets-1)
+    K kmin;
+    uint32_t shift;
+};
+
+template <class KT>
+struct KaryParams {
+    const KT* a;
+    uint64_t n;
+    const KT* sep;            // separator levels, top-first, node stride W (device)
+    uint32_t L;              // internal levels
+    uint32_t K;              // fan-out
+    uint32_t C;              // leaf chunk
+    uint32_t Ls;             // top levels staged in shared memory
+    uint32_t smem_bytes;     // bytes of sep staged (levels 0..Ls-1), 16-B multiple
+    uint64_t lvl_base[kMaxKaryLevels];   // element offset of level l (top-first)
+    uint32_t nodes_next[kMaxKaryLevels]; // node count of level l+1 (chunks for the last)
+    uint32_t stream_hint;
+    uint32_t leaf_hint;
+};
+
+// ---- launchers (return cudaGetLastError() after the launch) ----
+cudaError_t launch_naive(int kb, int ob, const void* a, uint64_t n, const void* q, uint64_t m,
+                         void* out, uint32_t threads, cudaStream_t s);
+
+// Grid: sched_static = 0 -> dynamic (one tile / warp-tile set per CTA on the
+// hardware scheduler); 1 -> persistent grid of sm_count x ctas_per_sm CTAs
+// (ctas_per_sm = 0: as many as are co-resident, from the occupancy API).
+struct Grid { uint32_t sched_static, ctas_per_sm, sm_count; };
+
+cudaError_t launch_opt(int kb, int ob, const void* params, const void* q, uint64_t m, void* out,
+                       uint32_t threads, uint32_t nreg, uint32_t reorder, Grid grid,
+                       uint32_t smem_bytes, cudaStream_t s, bool* unsupported);
+uint32_t opt_smem_extra(int kb, int ob, uint32_t threads, uint32_t nreg, uint32_t reorder);
+
+cudaError_t launch_kary(int kb, int ob, const void* params, const void* q, uint64_t m, void* out,
+                        uint32_t threads, uint32_t W, uint32_t R, Grid grid,
+                        uint32_t smem_bytes, cudaStream_t s, bool* unsupported);
+
+// ---- build kernels ----
+cudaError_t build_check_sorted(int kb, const void* a, uint64_t n, int* d_flag, cudaStream_t s);
+cudaError_t build_pinned_table(int kb, const void* a, uint64_t n, uint64_t s0, uint32_t nlev,
+                               const uint32_t* base, void* tab, uint64_t entries, cudaStream_t s);
+cudaError_t build_kary_levels(int kb, const void* a, uint64_t n, uint32_t K, uint32_t C, uint32_t W,
+                              uint32_t L, const uint64_t* lvl_base, const uint64_t* lvl_nodes,
+                              void* sep, uint64_t slots, cudaStream_t s);
+cudaError_t build_sort_keys(int kb, const void* in, void* out, uint64_t n, cudaStream_t s);
+
+// ---- multi-GPU routing kernels (dist.cu) ----
+cudaError_t launch_route(const uint64_t* q, uint64_t m, const uint64_t* shard_max, int P,
+                         uint32_t* dest, uint64_t* counts, cudaStream_t s);
+
+}  // namespace bs
