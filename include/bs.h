@@ -85,12 +85,15 @@ typedef struct {
     uint32_t leaf_chunk;    /* KARY leaf chunk C in keys, power of two 1..256       */
     uint32_t ctas_per_sm;   /* STATIC schedule: resident CTAs per SM; 0 = auto              */
     uint32_t cache_hints;   /* bitmask BS_HINT_*; 0 = plain loads/stores                    */
-    uint32_t reserved[7];   /* must be 0                                                    */
+    uint32_t kary_mode;     /* KARY: 1 = hybrid (thread per lookup in shared memory, W lanes per
+                               lookup in L2/HBM), 0 = W lanes per lookup at every level      */
+    uint32_t reserved[6];   /* must be 0                                                    */
 } bs_layout;
 
 /* cache_hints bits (B200 L2 eviction-priority hints; not in the paper) */
 #define BS_HINT_STREAM_EVICT_FIRST 1u  /* query loads / result stores: L2 evict_first    */
 #define BS_HINT_LEAF_EVICT_FIRST 2u    /* deepest probes / K-ary leaves: L2 evict_first  */
+#define BS_HINT_SEP_EVICT_LAST 4u      /* K-ary separator levels in global memory: L2 evict_last */
 
 /* Per-call launch override (bs_lookup_ex).  Only launch knobs; the structure
  * built by bs_build (pinned table size, K, C) is fixed.  Field meaning as in
@@ -106,7 +109,8 @@ typedef struct {
     uint32_t ctas_per_sm;
     uint32_t cache_hints;
     uint32_t use_pinned;    /* 1: use the pinned table / shared separator levels (if built) */
-    uint32_t reserved[6];
+    uint32_t kary_mode;     /* as bs_layout.kary_mode                                        */
+    uint32_t reserved[5];
 } bs_launch;
 
 typedef struct {

@@ -25,7 +25,7 @@ BS_OK, BS_ERR_INVALID, BS_ERR_UNSUPPORTED, BS_ERR_OOM, BS_ERR_CUDA, BS_ERR_NCCL,
 NAIVE, OPT, KARY = 0, 1, 2
 DYNAMIC, STATIC = 0, 1
 REORDER_NONE, REORDER_LOOKUP, REORDER_FULL = 0, 1, 2
-HINT_STREAM_EVICT_FIRST, HINT_LEAF_EVICT_FIRST = 1, 2
+HINT_STREAM_EVICT_FIRST, HINT_LEAF_EVICT_FIRST, HINT_SEP_EVICT_LAST = 1, 2, 4
 EXPORT_SORTED, EXPORT_PINNED, EXPORT_KARY = 0, 1, 2
 DIST_REPLICATED, DIST_PARTITIONED = 0, 1
 PIN_MAX = 0xFFFFFFFF
@@ -37,14 +37,14 @@ _u64 = ctypes.c_uint64
 class bs_layout(ctypes.Structure):
     _fields_ = [(f, _u32) for f in (
         "struct_size", "key_bytes", "out_bytes", "input_sorted", "variant", "schedule", "threads", "nreg",
-        "pin_bytes", "pin_partial", "reorder", "k", "leaf_chunk", "ctas_per_sm", "cache_hints")] + [
-        ("reserved", _u32 * 7)]
+        "pin_bytes", "pin_partial", "reorder", "k", "leaf_chunk", "ctas_per_sm", "cache_hints", "kary_mode")] + [
+        ("reserved", _u32 * 6)]
 
 
 class bs_launch(ctypes.Structure):
     _fields_ = [(f, _u32) for f in (
         "struct_size", "variant", "schedule", "threads", "nreg", "reorder", "pin_partial", "ctas_per_sm",
-        "cache_hints", "use_pinned")] + [("reserved", _u32 * 6)]
+        "cache_hints", "use_pinned", "kary_mode")] + [("reserved", _u32 * 5)]
 
 
 class bs_info(ctypes.Structure):

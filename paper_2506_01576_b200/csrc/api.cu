@@ -154,6 +154,7 @@ int bs_layout_default(bs_layout* l) {
     l->leaf_chunk = 16;
     l->ctas_per_sm = 0;
     l->cache_hints = BS_HINT_STREAM_EVICT_FIRST | BS_HINT_LEAF_EVICT_FIRST;
+    l->kary_mode = 1;
     return BS_OK;
 }
 
@@ -176,9 +177,10 @@ int bs_build(const void* keys, uint64_t n, const bs_layout* layout_in, void** ou
     if (lay.variant > BS_VARIANT_KARY) return fail(BS_ERR_INVALID, "unknown variant %u", lay.variant);
     if (lay.schedule > BS_SCHED_STATIC) return fail(BS_ERR_INVALID, "unknown schedule %u", lay.schedule);
     if (lay.reorder > BS_REORDER_FULL) return fail(BS_ERR_INVALID, "unknown reorder %u", lay.reorder);
+    if (lay.kary_mode > 1) return fail(BS_ERR_INVALID, "unknown kary_mode %u", lay.kary_mode);
     if (lay.k < 2 || lay.k > 33) return fail(BS_ERR_INVALID, "K must be in [2, 33]");
     if (!is_pow2(lay.leaf_chunk) || lay.leaf_chunk > 256) return fail(BS_ERR_INVALID, "leaf_chunk must be a power of two <= 256");
-    if (!reserved_zero(lay.reserved, 7)) return fail(BS_ERR_INVALID, "layout.reserved must be zero");
+    if (!reserved_zero(lay.reserved, 6)) return fail(BS_ERR_INVALID, "layout.reserved must be zero");
     if (lay.threads > 1024 || lay.threads % 32) return fail(BS_ERR_INVALID, "threads must be a multiple of 32 <= 1024");
 
     Index* ix = new Index();
@@ -209,8 +211,11 @@ int bs_build(const void* keys, uint64_t n, const bs_layout* layout_in, void** ou
     cudaEventRecord(e0, st);
 
     // ---- the sorted array ----
-    e = cudaMalloc(&ix->d_keys, abytes + 16);
+    // +256 keys of MAX padding: leaf chunks (C <= 256) may be read whole with vector loads
+    e = cudaMalloc(&ix->d_keys, abytes + 256 * ix->kb + 16);
     if (e != cudaSuccess) { rc = fail_cuda(e, "cudaMalloc(keys)"); goto done; }
+    e = cudaMemsetAsync((char*)ix->d_keys + abytes, 0xFF, 256 * ix->kb + 16, st);
+    if (e != cudaSuccess) { rc = fail_cuda(e, "memset(pad)"); goto done; }
     {
         cudaPointerAttributes pa;
         const bool dev = cudaPointerGetAttributes(&pa, keys) == cudaSuccess &&
@@ -308,6 +313,7 @@ int bs_launch_default(const void* idx, bs_launch* l) {
     l->ctas_per_sm = ix->layout.ctas_per_sm;
     l->cache_hints = ix->layout.cache_hints;
     l->use_pinned = ix->layout.pin_bytes != 0;
+    l->kary_mode = ix->layout.kary_mode;
     return BS_OK;
 }
 

@@ -83,10 +83,36 @@ __device__ __forceinline__ void stg_stream(uint32_t* p, uint32_t v, uint64_t pol
     asm volatile("st.global.L1::no_allocate.L2::cache_hint.u32 [%0], %1, %2;" :: "l"(p), "r"(v), "l"(pol) : "memory");
 }
 
-// Loads that pick the hinted or plain path from a runtime flag (uniform branch).
+// Random-access loads that do NOT allocate in L1: a plain ld.global.nc miss
+// makes L1 request the whole 128-B line from L2 (measured: 3.6 L2 sectors and
+// ~110 DRAM bytes per random 8-B load, tools/ubench_gather.cu), while
+// .L1::no_allocate requests only the touched sectors.
+__device__ __forceinline__ uint64_t ld_na(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.u64 %0, [%1];" : "=l"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ uint32_t ld_na(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ uint64_t ld_na_hint(const uint64_t* p, uint64_t pol) {
+    uint64_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ uint32_t ld_na_hint(const uint32_t* p, uint64_t pol) {
+    uint32_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+
+// Random probe of the sorted array / separator levels (no L1 allocation),
+// optionally with an L2 eviction-priority policy (uniform branch).
 template <class K>
 __device__ __forceinline__ K load_key(const K* p, bool hinted, uint64_t pol) {
-    return hinted ? ldg_hint(p, pol) : ldg(p);
+    return hinted ? ld_na_hint(p, pol) : ld_na(p);
 }
 template <class K>
 __device__ __forceinline__ K load_stream(const K* p, bool hinted, uint64_t pol) {

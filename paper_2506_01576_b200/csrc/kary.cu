@@ -36,24 +36,37 @@ __global__ void k_kary(const KaryParams<K> p, const K* __restrict__ q, uint64_t 
 
     if (p.smem_bytes) stage_to_smem(S, p.sep, p.smem_bytes, bar);
 
-    const uint64_t pol = policy_evict_first();
-    const bool sh = p.stream_hint != 0, lh = p.leaf_hint != 0;
+    const uint64_t pol_first = policy_evict_first();
+    const uint64_t pol_last = policy_evict_last();
+    const bool sh = p.stream_hint != 0, lh = p.leaf_hint != 0, sep_last = p.sep_hint != 0;
     const uint64_t n = p.n;
     const uint32_t K_ = p.K, C = p.C;
     const uint64_t warps_total = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    const uint64_t wid = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     constexpr uint32_t PER_WARP = GPW * R;
     const uint64_t nwt = (m + PER_WARP - 1) / PER_WARP;
+    uint64_t wt = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
 
-    for (uint64_t wt = wid; wt < nwt; wt += warps_total) {
+    // software pipeline: the queries of the next warp-tile are loaded while
+    // the current one descends (removes one DRAM round trip per lookup)
+    K knext[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const uint64_t i = wt * PER_WARP + (uint64_t)r * GPW + g;
+        knext[r] = (wt < nwt && i < m) ? load_stream(q + i, sh, pol_first) : KeyMax<K>::v;
+    }
+    for (; wt < nwt; wt += warps_total) {
         const uint64_t base = wt * PER_WARP;
         K key[R];
         uint32_t node[R];
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const uint64_t i = base + (uint64_t)r * GPW + g;
-            key[r] = (i < m) ? load_stream(q + i, sh, pol) : KeyMax<K>::v;
-            node[r] = 0;
+        for (int r = 0; r < R; ++r) { key[r] = knext[r]; node[r] = 0; }
+        {
+            const uint64_t wn = wt + warps_total;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const uint64_t i = wn * PER_WARP + (uint64_t)r * GPW + g;
+                knext[r] = (wn < nwt && i < m) ? load_stream(q + i, sh, pol_first) : KeyMax<K>::v;
+            }
         }
         // ---- internal levels: one node per group per level ----
         for (uint32_t l = 0; l < p.L; ++l) {
@@ -62,9 +75,12 @@ __global__ void k_kary(const KaryParams<K> p, const K* __restrict__ q, uint64_t 
             if (l < p.Ls) {
 #pragma unroll
                 for (int r = 0; r < R; ++r) s[r] = S[lb + (uint64_t)node[r] * W + j];
+            } else if (sep_last) {
+#pragma unroll
+                for (int r = 0; r < R; ++r) s[r] = ld_na_hint(p.sep + lb + (uint64_t)node[r] * W + j, pol_last);
             } else {
 #pragma unroll
-                for (int r = 0; r < R; ++r) s[r] = ldg(p.sep + lb + (uint64_t)node[r] * W + j);
+                for (int r = 0; r < R; ++r) s[r] = ld_na(p.sep + lb + (uint64_t)node[r] * W + j);
             }
             const uint32_t last = p.nodes_next[l] - 1;
 #pragma unroll
@@ -76,25 +92,25 @@ __global__ void k_kary(const KaryParams<K> p, const K* __restrict__ q, uint64_t 
             }
         }
         // ---- leaf chunk: lb = c*C + #{keys < q}, hit = any key == q ----
-        uint64_t cnt[R];
-        uint32_t hit[R];
+        uint32_t acc[R];   // (count << 1) | hit
 #pragma unroll
-        for (int r = 0; r < R; ++r) { cnt[r] = 0; hit[r] = 0; }
+        for (int r = 0; r < R; ++r) acc[r] = 0;
         for (uint32_t t0 = 0; t0 < C; t0 += W) {
             K x[R];
-            bool ok[R];
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 const uint64_t pos = (uint64_t)node[r] * C + t0 + j;
-                ok[r] = (t0 + j < C) && (pos < n);
-                x[r] = ok[r] ? load_key(p.a + pos, lh, pol) : KeyMax<K>::v;
+                const bool ok = (t0 + j < C) && (pos < n);
+                x[r] = ok ? load_key(p.a + pos, lh, pol_first) : KeyMax<K>::v;
             }
 #pragma unroll
             for (int r = 0; r < R; ++r) {
-                const uint32_t lt = __ballot_sync(0xFFFFFFFFu, ok[r] && x[r] < key[r]);
-                const uint32_t eq = __ballot_sync(0xFFFFFFFFu, ok[r] && x[r] == key[r]);
-                cnt[r] += __popc((lt >> gshift) & GMASK);
-                hit[r] |= (eq >> gshift) & GMASK;
+                const uint64_t pos = (uint64_t)node[r] * C + t0 + j;
+                const bool ok = (t0 + j < C) && (pos < n);
+                const uint32_t lt = __ballot_sync(0xFFFFFFFFu, ok && x[r] < key[r]);
+                const uint32_t eq = __ballot_sync(0xFFFFFFFFu, ok && x[r] == key[r]);
+                acc[r] += (uint32_t)__popc((lt >> gshift) & GMASK) << 1;
+                acc[r] |= ((eq >> gshift) & GMASK) ? 1u : 0u;
             }
         }
         if (j == 0) {
@@ -102,11 +118,11 @@ __global__ void k_kary(const KaryParams<K> p, const K* __restrict__ q, uint64_t 
             for (int r = 0; r < R; ++r) {
                 const uint64_t i = base + (uint64_t)r * GPW + g;
                 if (i < m) {
-                    uint64_t lbv = (uint64_t)node[r] * C + cnt[r];
+                    uint64_t lbv = (uint64_t)node[r] * C + (acc[r] >> 1);
                     if (lbv > n) lbv = n;
                     constexpr uint64_t MISS = 1ull << (8 * sizeof(O) - 1);
-                    const O res = (O)(hit[r] ? lbv : (lbv | MISS));
-                    store_stream(out + i, res, sh, pol);
+                    const O res = (O)((acc[r] & 1u) ? lbv : (lbv | MISS));
+                    store_stream(out + i, res, sh, pol_first);
                 }
             }
         }

@@ -121,10 +121,22 @@ static int run_kary(const Index* ix, const void* q, uint64_t m, void* out, cudaS
     p.smem_bytes = sbytes;
     p.stream_hint = (L.cache_hints & BS_HINT_STREAM_EVICT_FIRST) ? 1 : 0;
     p.leaf_hint = (L.cache_hints & BS_HINT_LEAF_EVICT_FIRST) ? 1 : 0;
+    p.sep_hint = (L.cache_hints & BS_HINT_SEP_EVICT_LAST) ? 1 : 0;
     const uint32_t smem = sbytes + 16;
     ix->last_kary_smem = smem;
     bool uns = false;
     Grid g{stat ? 1u : 0u, L.ctas_per_sm, (uint32_t)ix->sm_count};
+    const uint32_t W = ix->kW, C = ix->kC;
+    const uint32_t cpl = C >= W ? C / W : 1;
+    if (L.kary_mode == 1 && W <= 16 && cpl <= 4) {
+        // hybrid: nreg = waves in flight (a divisor of W); default all W waves (32 lookups / warp)
+        uint32_t I = L.nreg ? L.nreg : (W < 8 ? W : 8);
+        if (I > W) I = W;
+        cudaError_t e = launch_kary_hybrid(ix->kb, ix->ob, &p, q, m, out, threads, W, I, cpl, g, smem, s, &uns);
+        if (uns) return fail(BS_ERR_UNSUPPORTED, "KARY hybrid: threads=%u waves=%u W=%u C=%u not supported", threads, I, W, C);
+        if (e != cudaSuccess) return fail_cuda(e, "KARY hybrid launch");
+        return BS_OK;
+    }
     cudaError_t e = launch_kary(ix->kb, ix->ob, &p, q, m, out, threads, ix->kW, R, g, smem, s, &uns);
     if (uns) return fail(BS_ERR_UNSUPPORTED, "KARY: threads=%u waves=%u W=%u not supported", threads, R, ix->kW);
     if (e != cudaSuccess) return fail_cuda(e, "KARY launch");

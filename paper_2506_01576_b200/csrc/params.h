@@ -46,6 +46,7 @@ struct KaryParams {
     uint32_t nodes_next[kMaxKaryLevels]; // node count of level l+1 (chunks for the last)
     uint32_t stream_hint;
     uint32_t leaf_hint;
+    uint32_t sep_hint;       // 1: global separator levels with L2 evict_last
 };
 
 // ---- launchers (return cudaGetLastError() after the launch) ----
@@ -65,6 +66,11 @@ uint32_t opt_smem_extra(int kb, int ob, uint32_t threads, uint32_t nreg, uint32_
 cudaError_t launch_kary(int kb, int ob, const void* params, const void* q, uint64_t m, void* out,
                         uint32_t threads, uint32_t W, uint32_t R, Grid grid,
                         uint32_t smem_bytes, cudaStream_t s, bool* unsupported);
+
+// hybrid K-ary: I = waves in flight (divides W), cpl = leaf keys per lane (1, 2, 4)
+cudaError_t launch_kary_hybrid(int kb, int ob, const void* params, const void* q, uint64_t m, void* out,
+                               uint32_t threads, uint32_t W, uint32_t I, uint32_t cpl, Grid grid,
+                               uint32_t smem_bytes, cudaStream_t s, bool* unsupported);
 
 // ---- build kernels ----
 cudaError_t build_check_sorted(int kb, const void* a, uint64_t n, int* d_flag, cudaStream_t s);

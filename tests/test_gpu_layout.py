@@ -40,7 +40,7 @@ def test_pinned_table_matches_paper_positions(n):
         assert part == sorted(c.partial_positions, reverse=True)
 
 
-@pytest.mark.parametrize("n,K,C", [(27, 3, 3), (1000, 17, 16), (4097, 5, 4), (77777, 9, 8), (65536, 33, 32)])
+@pytest.mark.parametrize("n,K,C", [(27, 3, 4), (28, 3, 1), (1000, 17, 16), (4097, 5, 4), (77777, 9, 8), (65536, 33, 32)])
 def test_kary_levels_match_replay(n, K, C):
     """§5 separators = chunk maxima, levels top-first, child m*K+j; the
     device layout pads nodes to W = pow2 >= K-1 slots and levels to 128 B."""

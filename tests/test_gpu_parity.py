@@ -146,10 +146,11 @@ def test_kary_k_c_waves(kb):
     for K in (2, 3, 4, 5, 8, 9, 16, 17, 32, 33):
         for C in (1, 2, 4, 8, 16, 32, 64):
             idx = build(keys, variant=bs.KARY, k=K, leaf_chunk=C)
-            for R, sched, pin in ((1, bs.STATIC, 1), (2, bs.DYNAMIC, 0), (4, bs.STATIC, 0), (8, bs.STATIC, 1)):
-                got = run(idx, q, kb, variant=bs.KARY, nreg=R, schedule=sched, use_pinned=pin,
-                          threads=256 if R < 8 else 128)
-                check(got, want, q, f"K={K} C={C} R={R} sched={sched} pin={pin}")
+            for mode in (1, 0):
+                for R, sched, pin in ((1, bs.STATIC, 1), (2, bs.DYNAMIC, 0), (4, bs.STATIC, 0), (8, bs.STATIC, 1)):
+                    got = run(idx, q, kb, variant=bs.KARY, nreg=R, schedule=sched, use_pinned=pin,
+                              threads=256 if R < 8 else 128, kary_mode=mode)
+                    check(got, want, q, f"K={K} C={C} R={R} sched={sched} pin={pin} mode={mode}")
             idx.close()
 
 
@@ -160,7 +161,8 @@ def test_kary_small_n_all_shapes():
                 keys = edge_keys(n, 8, seed=n * 7 + K)
                 q = workload.adversarial_queries(keys, seed=K, extra=50)
                 idx = build(keys, variant=bs.KARY, k=K, leaf_chunk=C)
-                check(run(idx, q, 8), oracle.lookup(keys, q), q, f"n={n} K={K} C={C}")
+                for mode in (1, 0):
+                    check(run(idx, q, 8, kary_mode=mode), oracle.lookup(keys, q), q, f"n={n} K={K} C={C} mode={mode}")
 
 
 # ------------------------------------------------------------------ misc semantics
