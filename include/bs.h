@@ -85,8 +85,13 @@ typedef struct {
     uint32_t leaf_chunk;    /* KARY leaf chunk C in keys, power of two 1..256       */
     uint32_t ctas_per_sm;   /* STATIC schedule: resident CTAs per SM; 0 = auto              */
     uint32_t cache_hints;   /* bitmask BS_HINT_*; 0 = plain loads/stores                    */
-    uint32_t kary_mode;     /* KARY: 1 = hybrid (thread per lookup in shared memory, W lanes per
-                               lookup in L2/HBM), 0 = W lanes per lookup at every level      */
+    uint32_t kary_mode;     /* KARY schedule (same index, same results):
+                               0 = warp-cooperative: W lanes per lookup at every level;
+                               1 = hybrid: thread per lookup in shared memory (all W slots),
+                                   W lanes per lookup in L2/HBM;
+                               2 = tiered: thread per lookup with a binary search inside each
+                                   shared-memory node, W*key/16 lanes per lookup with 16-B
+                                   vector loads in L2/HBM (needs C/W in {1,2,4}, else mode 1) */
     uint32_t reserved[6];   /* must be 0                                                    */
 } bs_layout;
 

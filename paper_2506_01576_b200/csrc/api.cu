@@ -177,7 +177,7 @@ int bs_build(const void* keys, uint64_t n, const bs_layout* layout_in, void** ou
     if (lay.variant > BS_VARIANT_KARY) return fail(BS_ERR_INVALID, "unknown variant %u", lay.variant);
     if (lay.schedule > BS_SCHED_STATIC) return fail(BS_ERR_INVALID, "unknown schedule %u", lay.schedule);
     if (lay.reorder > BS_REORDER_FULL) return fail(BS_ERR_INVALID, "unknown reorder %u", lay.reorder);
-    if (lay.kary_mode > 1) return fail(BS_ERR_INVALID, "unknown kary_mode %u", lay.kary_mode);
+    if (lay.kary_mode > 2) return fail(BS_ERR_INVALID, "unknown kary_mode %u", lay.kary_mode);
     if (lay.k < 2 || lay.k > 33) return fail(BS_ERR_INVALID, "K must be in [2, 33]");
     if (!is_pow2(lay.leaf_chunk) || lay.leaf_chunk > 256) return fail(BS_ERR_INVALID, "leaf_chunk must be a power of two <= 256");
     if (!reserved_zero(lay.reserved, 6)) return fail(BS_ERR_INVALID, "layout.reserved must be zero");
@@ -327,6 +327,7 @@ int bs_lookup_ex(const void* idx, const void* queries, uint64_t m, void* out, vo
     } else {
         bs_launch_default(idx, &L);
     }
+    if (L.kary_mode > 2) return fail(BS_ERR_INVALID, "bs_lookup: unknown kary_mode %u", L.kary_mode);
     if (m == 0) return BS_OK;
     if (!queries || !out) return fail(BS_ERR_INVALID, "bs_lookup: NULL queries/out with m > 0");
     const uintptr_t q0 = (uintptr_t)queries, q1 = q0 + m * ix->kb;

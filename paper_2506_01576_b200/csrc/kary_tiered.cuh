@@ -1,0 +1,248 @@
+// kary_tiered.cuh — K-ary search (§5), "tiered" B200 schedule.
+//
+// Same index as kary.cu (chunk-max separators, top-first levels of W-slot
+// nodes, child m*K+j, leaf = the unpermuted sorted array; reading R16) and the
+// same result word.  Each tier of the memory hierarchy gets the schedule that
+// is cheapest there:
+//
+//  * shared-memory levels (the top Ls levels, staged once per CTA by TMA: the
+//    §5.1 "pinning" of KS): ONE thread per lookup, and the thread finds
+//    its child with a branch-free binary search inside the node
+//    (log2(W) dependent 8-B shared loads, +1 when K-1 == W) instead of reading
+//    all W slots — a node is sorted, so this is the same count of separators
+//    < q at a quarter of the shared-memory wavefronts.
+//  * global levels + leaf (L2 / HBM): G = W*key/16 lanes per lookup, each lane
+//    one 16-B vector load, so a node is ONE coalesced request of W*key bytes
+//    ("K-1 threads compare in parallel"; on B200 one 128-B line for
+//    K = 17 u64).  The group counts separators < q with one __ballot_sync per
+//    vector element and __popc.  A warp's 32 lookups are handed to its 32/G
+//    groups in G waves (__shfl_sync), I waves in flight at a time.
+//  * leaf: CPL = C/G keys per lane (R = C/W vector loads of 16 B); positions
+//    >= n read the MAX padding that bs_build writes and are masked out.
+//  * results are shuffled back to the owning lane and stored coalesced; the
+//    next warp-tile's queries are prefetched during the descent.
+#pragma once
+#include "common.cuh"
+#include "params.h"
+
+namespace bs {
+
+// V keys (V*sizeof(K) in {8, 16} bytes) from global memory, no L1 allocation,
+// optional L2 eviction-priority policy.
+template <class K, int V>
+__device__ __forceinline__ void ldv(const K* p, bool hint, uint64_t pol, K* x) {
+    if constexpr (sizeof(K) == 8) {
+        static_assert(V == 2, "u64: 16-B vectors");
+        if (hint)
+            asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u64 {%0,%1}, [%2], %3;"
+                         : "=l"(x[0]), "=l"(x[1]) : "l"(p), "l"(pol));
+        else
+            asm volatile("ld.global.nc.L1::no_allocate.v2.u64 {%0,%1}, [%2];" : "=l"(x[0]), "=l"(x[1]) : "l"(p));
+    } else if constexpr (V == 4) {
+        if (hint)
+            asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                         : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]) : "l"(p), "l"(pol));
+        else
+            asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]) : "l"(p));
+    } else {
+        static_assert(V == 2, "u32: 8- or 16-B vectors");
+        if (hint)
+            asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;"
+                         : "=r"(x[0]), "=r"(x[1]) : "l"(p), "l"(pol));
+        else
+            asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(x[0]), "=r"(x[1]) : "l"(p));
+    }
+}
+
+// #{slots < key} of one shared-memory node (W sorted slots, MAX-padded past
+// K-1), by branch-free binary search; `extra` = (K-1 == W) adds the final
+// compare that distinguishes "all W < key".
+template <class K, int W>
+__device__ __forceinline__ uint32_t smem_node_rank(const K* nd, K key, bool extra) {
+    uint32_t c = 0;
+#pragma unroll
+    for (int s = W / 2; s >= 1; s >>= 1) c += (nd[c + s - 1] < key) ? (uint32_t)s : 0u;
+    if (extra) c += (nd[c] < key) ? 1u : 0u;
+    return c;
+}
+
+template <class K, int W, int R, int I>
+__global__ void __launch_bounds__(1024, 1)
+k_kary_tiered(const KaryParams<K> p, const K* __restrict__ q, uint64_t m, void* __restrict__ out, uint32_t ob) {
+    constexpr int V = (16 / (int)sizeof(K)) < W ? (16 / (int)sizeof(K)) : W;   // keys per lane per load
+    constexpr int G = W / V;                                                  // lanes per lookup
+    constexpr int GPW = 32 / G;                                               // lookups per wave
+    constexpr int CPL = R * V;                                                // leaf keys per lane
+    constexpr uint32_t GMASK = (G == 32) ? 0xFFFFFFFFu : ((1u << G) - 1u);
+    static_assert(G >= 1 && 32 % G == 0 && G % I == 0, "bad tiered shape");
+
+    extern __shared__ __align__(16) unsigned char smem[];
+    K* S = reinterpret_cast<K*>(smem);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + p.smem_bytes);
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t j = lane % G;              // my lane within my group
+    const uint32_t g = lane / G;              // my group within the warp
+    const uint32_t gm = GMASK << (g * G);     // my group's lanes in a ballot
+    const uint32_t my_r = lane / GPW;         // wave that carries my own lookup
+    const uint32_t my_src = (lane % GPW) * G; // first lane of the group that carries it
+
+    if (p.smem_bytes) stage_to_smem(S, p.sep, p.smem_bytes, bar);
+
+    const uint64_t pol_first = policy_evict_first();
+    const uint64_t pol_last = policy_evict_last();
+    const bool sh = p.stream_hint != 0, lh = p.leaf_hint != 0, sep_last = p.sep_hint != 0;
+    const uint64_t n = p.n;
+    const uint32_t K_ = p.K, C = p.C, L = p.L, Ls = p.Ls;
+    const bool extra = (K_ - 1 == (uint32_t)W);
+    const uint64_t warps_total = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint64_t nwt = (m + 31) / 32;
+    uint64_t wt = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+
+    K knext = KeyMax<K>::v;
+    if (wt < nwt && wt * 32 + lane < m) knext = load_stream(q + wt * 32 + lane, sh, pol_first);
+
+    for (; wt < nwt; wt += warps_total) {
+        const K key = knext;
+        {
+            const uint64_t wn = wt + warps_total;
+            const uint64_t i = wn * 32 + lane;
+            knext = (wn < nwt && i < m) ? load_stream(q + i, sh, pol_first) : KeyMax<K>::v;
+        }
+        // ---- shared-memory levels: one thread per lookup, binary search in the node ----
+        uint32_t node = 0;
+        for (uint32_t l = 0; l < Ls; ++l) {
+            const uint32_t c = smem_node_rank<K, W>(S + p.lvl_base[l] + (uint64_t)node * W, key, extra);
+            const uint32_t child = node * K_ + c;
+            const uint32_t last = p.nodes_next[l] - 1;
+            node = child < last ? child : last;
+        }
+        // ---- global levels + leaf: G lanes per lookup, I waves in flight ----
+        uint64_t mine = 0;
+#pragma unroll 1
+        for (int b = 0; b < G / I; ++b) {
+            K kk[I];
+            uint32_t nn[I];
+#pragma unroll
+            for (int i = 0; i < I; ++i) {
+                const int src = (b * I + i) * GPW + (int)g;
+                kk[i] = __shfl_sync(0xFFFFFFFFu, key, src);
+                nn[i] = __shfl_sync(0xFFFFFFFFu, node, src);
+            }
+            for (uint32_t l = Ls; l < L; ++l) {
+                const K* lv = p.sep + p.lvl_base[l] + j * V;
+                K s[I][V];
+#pragma unroll
+                for (int i = 0; i < I; ++i) ldv<K, V>(lv + (uint64_t)nn[i] * W, sep_last, pol_last, s[i]);
+                const uint32_t last = p.nodes_next[l] - 1;
+#pragma unroll
+                for (int i = 0; i < I; ++i) {
+                    uint32_t c = 0;
+#pragma unroll
+                    for (int v = 0; v < V; ++v) c += __popc(__ballot_sync(0xFFFFFFFFu, s[i][v] < kk[i]) & gm);
+                    const uint32_t child = nn[i] * K_ + c;
+                    nn[i] = child < last ? child : last;
+                }
+            }
+            // leaf chunk c: lane j holds keys [c*C + j*CPL, +CPL) (MAX-padded past n)
+            K x[I][CPL];
+#pragma unroll
+            for (int i = 0; i < I; ++i) {
+                const K* lp = p.a + (uint64_t)nn[i] * C + j * CPL;
+#pragma unroll
+                for (int t = 0; t < R; ++t) ldv<K, V>(lp + t * V, lh, pol_first, &x[i][t * V]);
+            }
+#pragma unroll
+            for (int i = 0; i < I; ++i) {
+                const uint64_t p0 = (uint64_t)nn[i] * C + j * CPL;
+                uint32_t lt = 0;
+                bool eq = false;
+#pragma unroll
+                for (int t = 0; t < CPL; ++t) {
+                    const bool ok = p0 + t < n;
+                    lt += (ok && x[i][t] < kk[i]) ? 1u : 0u;
+                    eq |= ok && x[i][t] == kk[i];
+                }
+#pragma unroll
+                for (int o = G / 2; o > 0; o >>= 1) lt += __shfl_xor_sync(0xFFFFFFFFu, lt, o);
+                const bool hit = (__ballot_sync(0xFFFFFFFFu, eq) & gm) != 0;
+                uint64_t lbv = (uint64_t)nn[i] * C + lt;
+                if (lbv > n) lbv = n;
+                const uint64_t miss = ob == 8 ? (1ull << 63) : (1ull << 31);
+                const uint64_t res = hit ? lbv : (lbv | miss);
+                const uint64_t v = __shfl_sync(0xFFFFFFFFu, res, my_src);
+                if ((int)my_r == b * I + i) mine = v;
+            }
+        }
+        const uint64_t i = wt * 32 + lane;
+        if (i < m) {
+            if (ob == 8) store_stream((uint64_t*)out + i, mine, sh, pol_first);
+            else store_stream((uint32_t*)out + i, (uint32_t)mine, sh, pol_first);
+        }
+    }
+}
+
+template <class K, int W, int R, int I>
+static cudaError_t go_tiered(const void* params, const void* q, uint64_t m, void* out, uint32_t ob, uint32_t threads,
+                             Grid grid, uint32_t smem, cudaStream_t s, bool* uns) {
+    auto kern = k_kary_tiered<K, W, R, I>;
+    cudaFuncAttributes fa;
+    cudaError_t e = cudaFuncGetAttributes(&fa, kern);
+    if (e != cudaSuccess) return e;
+    if ((int)threads > fa.maxThreadsPerBlock || threads % 32) { *uns = true; return cudaSuccess; }
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const uint64_t per_cta = (uint64_t)threads;   // one lookup per thread per warp-tile
+    const uint64_t need = (m + per_cta - 1) / per_cta;
+    uint64_t g = need;
+    if (grid.sched_static) {
+        int occ = (int)grid.ctas_per_sm;
+        if (occ == 0) {
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, (int)threads, smem);
+            if (e != cudaSuccess) return e;
+        }
+        if (occ < 1) { *uns = true; return cudaSuccess; }
+        g = (uint64_t)grid.sm_count * (uint64_t)occ;
+    }
+    if (g > need) g = need;
+    if (g == 0) g = 1;
+    if (g > 0x7FFFFFFFull) g = 0x7FFFFFFFull;
+    kern<<<(unsigned)g, threads, smem, s>>>(*(const KaryParams<K>*)params, (const K*)q, m, out, ob);
+    return cudaGetLastError();
+}
+
+// W = node slots, R = C / W (1, 2, 4), I = waves in flight (clamped to a divisor of G)
+template <class K>
+cudaError_t dispatch_tiered(const void* params, const void* q, uint64_t m, void* out, uint32_t ob, uint32_t threads,
+                            uint32_t W, uint32_t R, uint32_t I, Grid grid, uint32_t smem, cudaStream_t s, bool* uns) {
+    constexpr int VK = 16 / (int)sizeof(K);
+#define BS_TI_I(WW, RR)                                                                                         \
+    {                                                                                                           \
+        constexpr int GG = WW / (VK < WW ? VK : WW);                                                            \
+        if (GG == 1 || I <= 1) return go_tiered<K, WW, RR, 1>(params, q, m, out, ob, threads, grid, smem, s, uns); \
+        if constexpr (GG >= 4) {                                                                                \
+            if (I >= 4) return go_tiered<K, WW, RR, 4>(params, q, m, out, ob, threads, grid, smem, s, uns);    \
+        }                                                                                                       \
+        if constexpr (GG >= 2) return go_tiered<K, WW, RR, 2>(params, q, m, out, ob, threads, grid, smem, s, uns); \
+    }
+#define BS_TI_R(WW)                          \
+    case WW:                                 \
+        if (R == 1) BS_TI_I(WW, 1)           \
+        if (R == 2) BS_TI_I(WW, 2)           \
+        if (R == 4) BS_TI_I(WW, 4)           \
+        break;
+    switch (W) {
+        BS_TI_R(2)
+        BS_TI_R(4)
+        BS_TI_R(8)
+        BS_TI_R(16)
+        BS_TI_R(32)
+        default: break;
+    }
+#undef BS_TI_R
+#undef BS_TI_I
+    *uns = true;
+    return cudaSuccess;
+}
+
+}  // namespace bs

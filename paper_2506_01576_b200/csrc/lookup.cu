@@ -109,7 +109,7 @@ static int run_kary(const Index* ix, const void* q, uint64_t m, void* out, cudaS
         p.lvl_base[l] = ix->k_base[l];
         p.nodes_next[l] = (uint32_t)ix->k_next[l];
     }
-    const uint32_t threads = L.threads ? L.threads : 512;
+    const uint32_t threads = L.threads ? L.threads : (L.kary_mode == 2 ? 1024 : 512);
     const uint32_t R = L.nreg ? L.nreg : 2;
     const bool stat = L.schedule == BS_SCHED_STATIC;
     uint32_t Ls = 0, sbytes = 0;
@@ -128,7 +128,15 @@ static int run_kary(const Index* ix, const void* q, uint64_t m, void* out, cudaS
     Grid g{stat ? 1u : 0u, L.ctas_per_sm, (uint32_t)ix->sm_count};
     const uint32_t W = ix->kW, C = ix->kC;
     const uint32_t cpl = C >= W ? C / W : 1;
-    if (L.kary_mode == 1 && W <= 16 && cpl <= 4) {
+    if (L.kary_mode == 2 && C >= W && (C / W == 1 || C / W == 2 || C / W == 4)) {
+        // tiered: nreg = waves in flight (default 4, clamped to a divisor of the group size)
+        const uint32_t I = L.nreg ? L.nreg : 4;
+        cudaError_t e = launch_kary_tiered(ix->kb, ix->ob, &p, q, m, out, threads, W, C / W, I, g, smem, s, &uns);
+        if (uns) return fail(BS_ERR_UNSUPPORTED, "KARY tiered: threads=%u W=%u C=%u not supported", threads, W, C);
+        if (e != cudaSuccess) return fail_cuda(e, "KARY tiered launch");
+        return BS_OK;
+    }
+    if (L.kary_mode >= 1 && W <= 16 && cpl <= 4) {
         // hybrid: nreg = waves in flight (a divisor of W); default all W waves (32 lookups / warp)
         uint32_t I = L.nreg ? L.nreg : (W < 8 ? W : 8);
         if (I > W) I = W;

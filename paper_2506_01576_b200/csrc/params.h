@@ -72,6 +72,13 @@ cudaError_t launch_kary_hybrid(int kb, int ob, const void* params, const void* q
                                uint32_t threads, uint32_t W, uint32_t I, uint32_t cpl, Grid grid,
                                uint32_t smem_bytes, cudaStream_t s, bool* unsupported);
 
+// tiered K-ary (kary_tiered.cuh): binary search inside shared-memory nodes,
+// 16-B vector loads by W*key/16 lanes per lookup below; R = C/W (1, 2, 4),
+// I = waves in flight; out word width ob passed at run time
+cudaError_t launch_kary_tiered(int kb, int ob, const void* params, const void* q, uint64_t m, void* out,
+                               uint32_t threads, uint32_t W, uint32_t R, uint32_t I, Grid grid, uint32_t smem,
+                               cudaStream_t s, bool* unsupported);
+
 // ---- build kernels ----
 cudaError_t build_check_sorted(int kb, const void* a, uint64_t n, int* d_flag, cudaStream_t s);
 cudaError_t build_pinned_table(int kb, const void* a, uint64_t n, uint64_t s0, uint32_t nlev,

@@ -31,6 +31,7 @@ ap.add_argument("--sched", type=int, default=1)
 ap.add_argument("--pin", type=int, default=1)
 ap.add_argument("--hints", type=int, default=3)
 ap.add_argument("--l2fetch", type=int, default=0)
+ap.add_argument("--mode", type=int, default=1, help="kary_mode: 1 hybrid, 0 warp-cooperative")
 a = ap.parse_args()
 torch.cuda.set_device(0)
 if a.l2fetch:
@@ -47,6 +48,6 @@ dq = P.as_torch(q)
 out = torch.empty(m, dtype={4: torch.int32, 8: torch.int64}[kb], device="cuda")
 for _ in range(a.launches):
     bs.bs_lookup_ex(idx, dq, m, out, None, variant=v, threads=a.threads, nreg=a.nreg, reorder=a.reorder,
-                    schedule=a.sched, use_pinned=a.pin, cache_hints=a.hints)
+                    schedule=a.sched, use_pinned=a.pin, cache_hints=a.hints, kary_mode=a.mode)
 torch.cuda.synchronize()
 print("done", idx.info)
