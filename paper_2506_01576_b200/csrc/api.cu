@@ -48,6 +48,7 @@ static void free_index(Index* ix) {
     if (ix->d_keys) cudaFree(ix->d_keys);
     if (ix->d_tab) cudaFree(ix->d_tab);
     if (ix->d_sep) cudaFree(ix->d_sep);
+    if (ix->d_img) cudaFree(ix->d_img);
     destroy_host_ctx(ix);
     destroy_dist_state(ix);
     delete ix;
@@ -121,6 +122,30 @@ static int build_kary_layout(Index* ix, cudaStream_t st) {
     if (e != cudaSuccess) return fail_cuda(e, "memset(separators)");
     e = build_kary_levels(kb, ix->d_keys, n, K, C, W, L, ix->k_base, ix->k_nodes, ix->d_sep, slot, st);
     if (e != cudaSuccess) return fail_cuda(e, "build_kary_levels");
+    // tiered shared-memory image: the longest level prefix whose planes fit one CTA's shared memory
+    {
+        // u64: hi plane below word 29056 (kary_tiered.cuh kImgLoWords), lo plane above it
+        const uint64_t cap_words = kb == 8 ? ((uint64_t)ix->smem_optin - 1024 - 16) / 4 - 29056 : ((uint64_t)ix->smem_optin - 1024 - 16) / 4;
+        uint32_t words = 0, Li = 0;
+        for (uint32_t l = 0; l < L; ++l) {
+            const uint64_t w = ((ix->k_nodes[l] * (W + 1) + 3) / 4) * 4;   // 16-B multiple per level
+            if (words + w > cap_words) break;
+            ix->img_base[l] = words;
+            words += (uint32_t)w;
+            ++Li;
+        }
+        ix->img_base[Li] = words;
+        ix->img_L = Li;
+        if (Li > 0) {
+            const uint64_t planes = (kb == 8) ? 2 : 1;
+            e = cudaMalloc(&ix->d_img, (uint64_t)words * 4 * planes);
+            if (e != cudaSuccess) return fail_cuda(e, "cudaMalloc(shared image)");
+            uint64_t nodes[kMaxKaryLevels];
+            for (uint32_t l = 0; l < Li; ++l) nodes[l] = ix->k_nodes[l];
+            e = build_kary_image(kb, ix->d_sep, W, Li, ix->k_base, nodes, ix->img_base, words, ix->d_img, st);
+            if (e != cudaSuccess) return fail_cuda(e, "build_kary_image");
+        }
+    }
     return BS_OK;
 }
 
@@ -365,6 +390,7 @@ int bs_index_info(const void* idx, bs_info* info) {
     info->separator_bytes = info->separator_slots * ix->kb;
     info->kary_smem_levels = ix->kary_built ? kary_smem_levels(ix, nullptr) : 0;
     info->footprint_bytes = info->array_bytes + ix->tab_entries * ix->kb + info->separator_bytes;
+    if (ix->d_img) info->footprint_bytes += (uint64_t)ix->img_base[ix->img_L] * 4 * (ix->kb == 8 ? 2 : 1);
     info->build_ms = ix->build_ms;
     info->sm_count = ix->sm_count;
     info->smem_per_cta_opt = (uint32_t)ix->last_opt_smem;

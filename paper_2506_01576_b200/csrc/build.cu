@@ -115,6 +115,55 @@ cudaError_t build_kary_levels(int kb, const void* a, uint64_t n, uint32_t Kf, ui
     return cudaGetLastError();
 }
 
+struct ImgMeta {
+    uint64_t sep_base[kMaxKaryLevels];
+    uint64_t start[kMaxKaryLevels + 1];   // cumulative image slots (node*(W+1)) per level
+    uint32_t img_base[kMaxKaryLevels];
+};
+
+// Tiered shared-memory image: slot s of node m of level l -> word
+// img_base[l] + m*(W+1) + s of each plane; s == W is padding.
+template <class K>
+__global__ void k_build_img(const K* __restrict__ sep, uint32_t W, uint32_t L, ImgMeta meta, uint32_t* __restrict__ img,
+                            uint64_t plane_words) {
+    const uint64_t total = meta.start[L];
+    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t l = 0;
+        while (l + 1 < L && meta.start[l + 1] <= e) ++l;
+        const uint64_t rel = e - meta.start[l];
+        const uint64_t node = rel / (W + 1), s = rel % (W + 1);
+        const K v = (s < W) ? sep[meta.sep_base[l] + node * W + s] : KeyMax<K>::v;
+        const uint64_t w = meta.img_base[l] + rel;
+        if constexpr (sizeof(K) == 8) {
+            img[w] = (uint32_t)((uint64_t)v >> 32);
+            img[plane_words + w] = (uint32_t)v;
+        } else {
+            img[w] = (uint32_t)v;
+        }
+    }
+}
+
+cudaError_t build_kary_image(int kb, const void* sep, uint32_t W, uint32_t L, const uint64_t* lvl_base,
+                              const uint64_t* lvl_nodes, const uint32_t* img_base, uint64_t plane_words,
+                              void* img, cudaStream_t s) {
+    if (L == 0) return cudaSuccess;
+    ImgMeta meta;
+    uint64_t acc = 0;
+    for (uint32_t l = 0; l < L; ++l) {
+        meta.sep_base[l] = lvl_base[l];
+        meta.img_base[l] = img_base[l];
+        meta.start[l] = acc;
+        acc += lvl_nodes[l] * (W + 1);
+    }
+    meta.start[L] = acc;
+    if (kb == 8)
+        k_build_img<uint64_t><<<grid_for(acc, 256), 256, 0, s>>>((const uint64_t*)sep, W, L, meta, (uint32_t*)img, plane_words);
+    else
+        k_build_img<uint32_t><<<grid_for(acc, 256), 256, 0, s>>>((const uint32_t*)sep, W, L, meta, (uint32_t*)img, plane_words);
+    return cudaGetLastError();
+}
+
 cudaError_t build_sort_keys(int kb, const void* in, void* out, uint64_t n, cudaStream_t s) {
     size_t tmp_bytes = 0;
     cudaError_t e;

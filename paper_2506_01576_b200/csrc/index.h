@@ -38,6 +38,14 @@ struct Index {
     uint64_t k_nodes[kMaxKaryLevels] = {};
     uint64_t k_next[kMaxKaryLevels] = {};
     uint64_t sep_slots = 0;
+    // shared-memory image of the top K-ary levels for the tiered schedule:
+    // node stride W+1 words (odd: lanes in different nodes reading the same
+    // slot fall in different banks); u64 split into a hi-word and a lo-word
+    // plane so a probe is one 4-B shared load (the lo word is read only when
+    // the hi words tie).  img_base[l] = word offset of level l in a plane.
+    void* d_img = nullptr;
+    uint32_t img_L = 0;
+    uint32_t img_base[kMaxKaryLevels + 1] = {};
 
     // device
     int sm_count = 148, smem_optin = 232448, smem_per_sm = 233472, l2_bytes = 0;

@@ -55,16 +55,59 @@ __device__ __forceinline__ void ldv(const K* p, bool hint, uint64_t pol, K* x) {
     }
 }
 
+// slot < key for a slot of the shared-memory image: u32 keys read the one
+// plane; u64 keys read the hi-word plane and, only when the hi words tie, the
+// lo-word plane (one 4-B bank access per probe).
+// The lo plane sits at a fixed shared-memory offset so its probe is the hi
+// probe's address plus an immediate.
+constexpr uint32_t kImgLoWords = 29056;   // 116224 B = half of sm_100's 227 KB opt-in
+
+template <class K>
+__device__ __forceinline__ bool img_less(const uint32_t* S, uint32_t w, K key) {
+    if constexpr (sizeof(K) == 8) {
+        const uint32_t qh = (uint32_t)((uint64_t)key >> 32);
+        const uint32_t h = S[w];
+        bool less = h < qh;
+        if (h == qh) less = S[kImgLoWords + w] < (uint32_t)key;
+        return less;
+    } else {
+        return S[w] < (uint32_t)key;
+    }
+}
+
 // #{slots < key} of one shared-memory node (W sorted slots, MAX-padded past
-// K-1), by branch-free binary search; `extra` = (K-1 == W) adds the final
-// compare that distinguishes "all W < key".
+// K-1), by branch-free binary search over the image; `extra` = (K-1 == W)
+// adds the final compare that distinguishes "all W < key".
 template <class K, int W>
-__device__ __forceinline__ uint32_t smem_node_rank(const K* nd, K key, bool extra) {
+__device__ __forceinline__ uint32_t smem_node_rank(const uint32_t* S, uint32_t nd, K key, bool extra) {
     uint32_t c = 0;
 #pragma unroll
-    for (int s = W / 2; s >= 1; s >>= 1) c += (nd[c + s - 1] < key) ? (uint32_t)s : 0u;
-    if (extra) c += (nd[c] < key) ? 1u : 0u;
+    for (int s = W / 2; s >= 1; s >>= 1) c += img_less<K>(S, nd + c + s - 1, key) ? (uint32_t)s : 0u;
+    if (extra) c += img_less<K>(S, nd + c, key) ? 1u : 0u;
     return c;
+}
+
+// Stage the first `words` words of each image plane with TMA bulk copies:
+// hi (or the u32 plane) at word 0, lo at word kImgLoWords.
+template <class K>
+__device__ __forceinline__ void stage_image(uint32_t* S, const uint32_t* img, uint64_t plane_words, uint32_t words,
+                                            uint64_t* bar) {
+    constexpr uint32_t planes = sizeof(K) == 8 ? 2 : 1;
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        mbar_arrive_expect_tx(bar, words * 4 * planes);
+        constexpr uint32_t CH = 32768;
+        for (uint32_t pl = 0; pl < planes; ++pl)
+            for (uint32_t o = 0; o < words * 4; o += CH) {
+                const uint32_t b = (words * 4 - o < CH) ? (words * 4 - o) : CH;
+                bulk_g2s((char*)(S + pl * kImgLoWords) + o, (const char*)(img + pl * plane_words) + o, b, bar);
+            }
+    }
+    mbar_wait(bar, 0);
 }
 
 template <class K, int W, int R, int I>
@@ -78,8 +121,8 @@ k_kary_tiered(const KaryParams<K> p, const K* __restrict__ q, uint64_t m, void* 
     static_assert(G >= 1 && 32 % G == 0 && G % I == 0, "bad tiered shape");
 
     extern __shared__ __align__(16) unsigned char smem[];
-    K* S = reinterpret_cast<K*>(smem);
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + p.smem_bytes);
+    uint32_t* S = reinterpret_cast<uint32_t*>(smem);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + p.smem_bytes - 16);
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t j = lane % G;              // my lane within my group
     const uint32_t g = lane / G;              // my group within the warp
@@ -87,7 +130,7 @@ k_kary_tiered(const KaryParams<K> p, const K* __restrict__ q, uint64_t m, void* 
     const uint32_t my_r = lane / GPW;         // wave that carries my own lookup
     const uint32_t my_src = (lane % GPW) * G; // first lane of the group that carries it
 
-    if (p.smem_bytes) stage_to_smem(S, p.sep, p.smem_bytes, bar);
+    if (p.img_words) stage_image<K>(S, p.img, p.img_plane_words, p.img_words, bar);
 
     const uint64_t pol_first = policy_evict_first();
     const uint64_t pol_last = policy_evict_last();
@@ -112,7 +155,7 @@ k_kary_tiered(const KaryParams<K> p, const K* __restrict__ q, uint64_t m, void* 
         // ---- shared-memory levels: one thread per lookup, binary search in the node ----
         uint32_t node = 0;
         for (uint32_t l = 0; l < Ls; ++l) {
-            const uint32_t c = smem_node_rank<K, W>(S + p.lvl_base[l] + (uint64_t)node * W, key, extra);
+            const uint32_t c = smem_node_rank<K, W>(S, p.img_base[l] + node * (W + 1), key, extra);
             const uint32_t child = node * K_ + c;
             const uint32_t last = p.nodes_next[l] - 1;
             node = child < last ? child : last;

@@ -47,6 +47,11 @@ struct KaryParams {
     uint32_t stream_hint;
     uint32_t leaf_hint;
     uint32_t sep_hint;       // 1: global separator levels with L2 evict_last
+    // tiered schedule: shared-memory image (Index::d_img), levels 0..Ls-1
+    const uint32_t* img;     // hi plane (u64) / the plane (u32), then the lo plane
+    uint64_t img_plane_words;// words per plane in global memory
+    uint32_t img_base[kMaxKaryLevels];
+    uint32_t img_words;      // words of each plane staged (img_base[Ls], 4-word multiple)
 };
 
 // ---- launchers (return cudaGetLastError() after the launch) ----
@@ -86,6 +91,9 @@ cudaError_t build_pinned_table(int kb, const void* a, uint64_t n, uint64_t s0, u
 cudaError_t build_kary_levels(int kb, const void* a, uint64_t n, uint32_t K, uint32_t C, uint32_t W,
                               uint32_t L, const uint64_t* lvl_base, const uint64_t* lvl_nodes,
                               void* sep, uint64_t slots, cudaStream_t s);
+cudaError_t build_kary_image(int kb, const void* sep, uint32_t W, uint32_t L, const uint64_t* lvl_base,
+                              const uint64_t* lvl_nodes, const uint32_t* img_base, uint64_t plane_words,
+                              void* img, cudaStream_t s);
 cudaError_t build_sort_keys(int kb, const void* in, void* out, uint64_t n, cudaStream_t s);
 
 // ---- multi-GPU routing kernels (dist.cu) ----
