@@ -60,47 +60,59 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons during the timed region."""
+    """nvidia-smi clocks + throttle reasons DURING the timed region: one
+    `nvidia-smi -lms 20` process streams samples from before the first timed
+    launch until after the last (B200_PROFILING.md clocks line)."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,power.draw")
 
     def __init__(self, dev: int):
         self.dev = dev
         self.samples = []
-        self._stop = threading.Event()
+        self._p = None
         self._t = None
 
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.1)
+    def _read(self):
+        for line in self._p.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 6:
+                self.samples.append(parts)
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        try:
+            self._p = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}",
+                                        "--format=csv,noheader,nounits", "-lms", "20"],
+                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+            time.sleep(0.05)
+        except Exception:
+            self._p = None
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        self._t.join(timeout=10)
+        if self._p is not None:
+            time.sleep(0.03)
+            self._p.terminate()
+            try:
+                self._p.wait(timeout=5)
+            except Exception:
+                self._p.kill()
+            self._t.join(timeout=5)
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        num = lambda x: float(x) if x.replace(".", "", 1).isdigit() else None  # noqa: E731
+        sm = [num(s[0]) for s in self.samples if num(s[0]) is not None]
+        mx = [num(s[1]) for s in self.samples if num(s[1]) is not None]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        pw = [num(s[6]) for s in self.samples if len(s) > 6 and num(s[6]) is not None]
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+                "reasons": reasons, "samples": len(self.samples),
+                "power_w_max": max(pw) if pw else None}
 
 
 def make_inputs(cfg: str, order: str, rank: int):
@@ -161,7 +173,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="config3", choices=sorted(CONFIGS))
@@ -174,6 +186,7 @@ def main():
     ap.add_argument("--reorder", type=int, default=0)
     ap.add_argument("--schedule", type=int, default=1)
     ap.add_argument("--hints", type=int, default=3)
+    ap.add_argument("--kary-mode", type=int, default=2, help="0 warp, 1 hybrid, 2 tiered, 3 tiered 8-B probes")
     ap.add_argument("--no-naive", action="store_true", help="skip the naive comparison leg")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=1 << 22)
@@ -204,11 +217,12 @@ def main():
     dq = P.as_torch(q)
     out = torch.empty(m, dtype={4: torch.int32, 8: torch.int64}[ob], device="cuda")
 
-    K = args.k or (17 if kb == 8 else 17)
-    C = args.leaf_chunk or (16 if kb == 8 else 32)
+    K = args.k or 9
+    C = args.leaf_chunk or 16
     lay = bs.bs_layout_default(key_bytes=kb, out_bytes=ob, variant=VARIANTS[args.variant], k=K, leaf_chunk=C,
                                schedule=args.schedule, threads=args.threads, nreg=args.nreg,
-                               reorder=args.reorder, cache_hints=args.hints)
+                               reorder=args.reorder, cache_hints=args.hints,
+                               kary_mode=args.kary_mode)
     idx = bs.bs_build(dk, n, lay)
     del dk
     stream = torch.cuda.Stream()
@@ -287,7 +301,7 @@ def main():
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         tj = json.load(open(tp))
-        key = f"{args.config}/{args.order}/{args.variant}"
+        key = f"{args.config}/{args.order}/{args.variant}/K{K}/C{C}/mode{args.kary_mode}"
         if key in tj:
             traffic = tj[key]["dram_bytes_per_launch"]
     info = idx.info
@@ -301,7 +315,8 @@ def main():
                    "parallelism": f"replicated x{world}" if world > 1 else "1 GPU",
                    "l2": "inputs larger than L2 (queries+results 2 GiB per step > 126 MB), no flush"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "bytes_per_lookup_alg": bpl, "peak_source": peak_src},
+                     "traffic": traffic, "traffic_unit": "DRAM bytes per launch (ncu --set full)",
+                     "alg_bytes_per_launch": bpl * m, "bytes_per_lookup_alg": bpl, "peak_source": peak_src},
         "gpu_launches": args.steps,
         "clocks": clocks,
         "parity_sample_ok": parity_ok,

@@ -81,7 +81,7 @@ typedef struct {
                                0xFFFFFFFF = largest that fits                              */
     uint32_t pin_partial;   /* OPT: 1 = "full-pinning" (partial step M+1), 0 = "steps-pinning" */
     uint32_t reorder;       /* bs_reorder (OPT only)                                        */
-    uint32_t k;             /* KARY fan-out K, 2..33 (P:213, P:223 best K = 17)             */
+    uint32_t k;             /* KARY fan-out K, 2..33 (P:223 A6000 best K = 17)       */
     uint32_t leaf_chunk;    /* KARY leaf chunk C in keys, power of two 1..256       */
     uint32_t ctas_per_sm;   /* STATIC schedule: resident CTAs per SM; 0 = auto              */
     uint32_t cache_hints;   /* bitmask BS_HINT_*; 0 = plain loads/stores                    */
@@ -91,7 +91,9 @@ typedef struct {
                                    W lanes per lookup in L2/HBM;
                                2 = tiered: thread per lookup with a binary search inside each
                                    shared-memory node, W*key/16 lanes per lookup with 16-B
-                                   vector loads in L2/HBM (needs C/W in {1,2,4}, else mode 1) */
+                                   vector loads in L2/HBM (needs C/W in {1,2,4}, else mode 1);
+                               3 = tiered with 8-B shared probes (u64: one slot plane instead
+                                   of hi/lo word planes; u32: same as 2)                     */
     uint32_t reserved[6];   /* must be 0                                                    */
 } bs_layout;
 
@@ -145,8 +147,10 @@ typedef struct {
 #define BS_EXPORT_PINNED 1   /* the level-major pinned table (pinned_entries keys)     */
 #define BS_EXPORT_KARY 2     /* K-ary separator slots, levels top-first (separator_slots) */
 
-/* Fills *l with defaults for u64 keys/outputs, K-ary K = 17 / C = 16, largest
- * pin budget, static schedule.  BS_ERR_INVALID if l is NULL. */
+/* Fills *l with defaults for u64 keys/outputs, K-ary K = 9 / C = 16 with the
+ * tiered schedule (kary_mode 2; the fastest measured on B200 for 2^26 u64 keys,
+ * the paper's A6000 optimum was K = 17), largest pin
+ * budget, static schedule.  BS_ERR_INVALID if l is NULL. */
 int bs_layout_default(bs_layout* l);
 
 /* Fills *l with the per-call defaults stored in idx. */

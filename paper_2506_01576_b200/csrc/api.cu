@@ -49,6 +49,7 @@ static void free_index(Index* ix) {
     if (ix->d_tab) cudaFree(ix->d_tab);
     if (ix->d_sep) cudaFree(ix->d_sep);
     if (ix->d_img) cudaFree(ix->d_img);
+    if (ix->d_img64) cudaFree(ix->d_img64);
     destroy_host_ctx(ix);
     destroy_dist_state(ix);
     delete ix;
@@ -142,8 +143,29 @@ static int build_kary_layout(Index* ix, cudaStream_t st) {
             if (e != cudaSuccess) return fail_cuda(e, "cudaMalloc(shared image)");
             uint64_t nodes[kMaxKaryLevels];
             for (uint32_t l = 0; l < Li; ++l) nodes[l] = ix->k_nodes[l];
-            e = build_kary_image(kb, ix->d_sep, W, Li, ix->k_base, nodes, ix->img_base, words, ix->d_img, st);
+            e = build_kary_image(kb, ix->d_sep, W, Li, ix->k_base, nodes, ix->img_base, words, ix->d_img, false, st);
             if (e != cudaSuccess) return fail_cuda(e, "build_kary_image");
+        }
+    }
+    if (kb == 8) {   // 8-B-slot image (kary_mode 3)
+        const uint64_t cap_slots = ((uint64_t)ix->smem_optin - 1024 - 16) / 8;
+        uint32_t slots = 0, Li = 0;
+        for (uint32_t l = 0; l < L; ++l) {
+            const uint64_t w = ((ix->k_nodes[l] * (W + 1) + 1) / 2) * 2;   // 16-B multiple per level
+            if (slots + w > cap_slots) break;
+            ix->img64_base[l] = slots;
+            slots += (uint32_t)w;
+            ++Li;
+        }
+        ix->img64_base[Li] = slots;
+        ix->img64_L = Li;
+        if (Li > 0) {
+            e = cudaMalloc(&ix->d_img64, (uint64_t)slots * 8);
+            if (e != cudaSuccess) return fail_cuda(e, "cudaMalloc(shared image 64)");
+            uint64_t nodes[kMaxKaryLevels];
+            for (uint32_t l = 0; l < Li; ++l) nodes[l] = ix->k_nodes[l];
+            e = build_kary_image(kb, ix->d_sep, W, Li, ix->k_base, nodes, ix->img64_base, slots, ix->d_img64, true, st);
+            if (e != cudaSuccess) return fail_cuda(e, "build_kary_image(64)");
         }
     }
     return BS_OK;
@@ -175,11 +197,11 @@ int bs_layout_default(bs_layout* l) {
     l->pin_bytes = 0xFFFFFFFFu;
     l->pin_partial = 1;
     l->reorder = BS_REORDER_NONE;
-    l->k = 17;
+    l->k = 9;
     l->leaf_chunk = 16;
     l->ctas_per_sm = 0;
     l->cache_hints = BS_HINT_STREAM_EVICT_FIRST | BS_HINT_LEAF_EVICT_FIRST;
-    l->kary_mode = 1;
+    l->kary_mode = 2;
     return BS_OK;
 }
 
@@ -202,7 +224,7 @@ int bs_build(const void* keys, uint64_t n, const bs_layout* layout_in, void** ou
     if (lay.variant > BS_VARIANT_KARY) return fail(BS_ERR_INVALID, "unknown variant %u", lay.variant);
     if (lay.schedule > BS_SCHED_STATIC) return fail(BS_ERR_INVALID, "unknown schedule %u", lay.schedule);
     if (lay.reorder > BS_REORDER_FULL) return fail(BS_ERR_INVALID, "unknown reorder %u", lay.reorder);
-    if (lay.kary_mode > 2) return fail(BS_ERR_INVALID, "unknown kary_mode %u", lay.kary_mode);
+    if (lay.kary_mode > 3) return fail(BS_ERR_INVALID, "unknown kary_mode %u", lay.kary_mode);
     if (lay.k < 2 || lay.k > 33) return fail(BS_ERR_INVALID, "K must be in [2, 33]");
     if (!is_pow2(lay.leaf_chunk) || lay.leaf_chunk > 256) return fail(BS_ERR_INVALID, "leaf_chunk must be a power of two <= 256");
     if (!reserved_zero(lay.reserved, 6)) return fail(BS_ERR_INVALID, "layout.reserved must be zero");
@@ -352,7 +374,7 @@ int bs_lookup_ex(const void* idx, const void* queries, uint64_t m, void* out, vo
     } else {
         bs_launch_default(idx, &L);
     }
-    if (L.kary_mode > 2) return fail(BS_ERR_INVALID, "bs_lookup: unknown kary_mode %u", L.kary_mode);
+    if (L.kary_mode > 3) return fail(BS_ERR_INVALID, "bs_lookup: unknown kary_mode %u", L.kary_mode);
     if (m == 0) return BS_OK;
     if (!queries || !out) return fail(BS_ERR_INVALID, "bs_lookup: NULL queries/out with m > 0");
     const uintptr_t q0 = (uintptr_t)queries, q1 = q0 + m * ix->kb;
@@ -391,6 +413,7 @@ int bs_index_info(const void* idx, bs_info* info) {
     info->kary_smem_levels = ix->kary_built ? kary_smem_levels(ix, nullptr) : 0;
     info->footprint_bytes = info->array_bytes + ix->tab_entries * ix->kb + info->separator_bytes;
     if (ix->d_img) info->footprint_bytes += (uint64_t)ix->img_base[ix->img_L] * 4 * (ix->kb == 8 ? 2 : 1);
+    if (ix->d_img64) info->footprint_bytes += (uint64_t)ix->img64_base[ix->img64_L] * 8;
     info->build_ms = ix->build_ms;
     info->sm_count = ix->sm_count;
     info->smem_per_cta_opt = (uint32_t)ix->last_opt_smem;

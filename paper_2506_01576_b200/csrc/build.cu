@@ -123,7 +123,7 @@ struct ImgMeta {
 
 // Tiered shared-memory image: slot s of node m of level l -> word
 // img_base[l] + m*(W+1) + s of each plane; s == W is padding.
-template <class K>
+template <class K, bool PAIR>
 __global__ void k_build_img(const K* __restrict__ sep, uint32_t W, uint32_t L, ImgMeta meta, uint32_t* __restrict__ img,
                             uint64_t plane_words) {
     const uint64_t total = meta.start[L];
@@ -135,7 +135,9 @@ __global__ void k_build_img(const K* __restrict__ sep, uint32_t W, uint32_t L, I
         const uint64_t node = rel / (W + 1), s = rel % (W + 1);
         const K v = (s < W) ? sep[meta.sep_base[l] + node * W + s] : KeyMax<K>::v;
         const uint64_t w = meta.img_base[l] + rel;
-        if constexpr (sizeof(K) == 8) {
+        if constexpr (PAIR) {
+            reinterpret_cast<uint64_t*>(img)[w] = (uint64_t)v;
+        } else if constexpr (sizeof(K) == 8) {
             img[w] = (uint32_t)((uint64_t)v >> 32);
             img[plane_words + w] = (uint32_t)v;
         } else {
@@ -146,7 +148,7 @@ __global__ void k_build_img(const K* __restrict__ sep, uint32_t W, uint32_t L, I
 
 cudaError_t build_kary_image(int kb, const void* sep, uint32_t W, uint32_t L, const uint64_t* lvl_base,
                               const uint64_t* lvl_nodes, const uint32_t* img_base, uint64_t plane_words,
-                              void* img, cudaStream_t s) {
+                              void* img, bool pair64, cudaStream_t s) {
     if (L == 0) return cudaSuccess;
     ImgMeta meta;
     uint64_t acc = 0;
@@ -157,10 +159,12 @@ cudaError_t build_kary_image(int kb, const void* sep, uint32_t W, uint32_t L, co
         acc += lvl_nodes[l] * (W + 1);
     }
     meta.start[L] = acc;
-    if (kb == 8)
-        k_build_img<uint64_t><<<grid_for(acc, 256), 256, 0, s>>>((const uint64_t*)sep, W, L, meta, (uint32_t*)img, plane_words);
+    if (kb == 8 && pair64)
+        k_build_img<uint64_t, true><<<grid_for(acc, 256), 256, 0, s>>>((const uint64_t*)sep, W, L, meta, (uint32_t*)img, plane_words);
+    else if (kb == 8)
+        k_build_img<uint64_t, false><<<grid_for(acc, 256), 256, 0, s>>>((const uint64_t*)sep, W, L, meta, (uint32_t*)img, plane_words);
     else
-        k_build_img<uint32_t><<<grid_for(acc, 256), 256, 0, s>>>((const uint32_t*)sep, W, L, meta, (uint32_t*)img, plane_words);
+        k_build_img<uint32_t, false><<<grid_for(acc, 256), 256, 0, s>>>((const uint32_t*)sep, W, L, meta, (uint32_t*)img, plane_words);
     return cudaGetLastError();
 }
 

@@ -46,6 +46,11 @@ struct Index {
     void* d_img = nullptr;
     uint32_t img_L = 0;
     uint32_t img_base[kMaxKaryLevels + 1] = {};
+    // u64 only: the same image as whole 8-B slots (one plane, node stride W+1
+    // slots): one dependent shared load per probe instead of hi then lo
+    void* d_img64 = nullptr;
+    uint32_t img64_L = 0;
+    uint32_t img64_base[kMaxKaryLevels + 1] = {};
 
     // device
     int sm_count = 148, smem_optin = 232448, smem_per_sm = 233472, l2_bytes = 0;

@@ -19,8 +19,8 @@
 //    groups in G waves (__shfl_sync), I waves in flight at a time.
 //  * leaf: CPL = C/G keys per lane (R = C/W vector loads of 16 B); positions
 //    >= n read the MAX padding that bs_build writes and are masked out.
-//  * results are shuffled back to the owning lane and stored coalesced; the
-//    next warp-tile's queries are prefetched during the descent.
+//  * each group's first lane stores its result (a wave's 32/G results are
+//    contiguous); the next warp-tile's queries are prefetched during the descent.
 #pragma once
 #include "common.cuh"
 #include "params.h"
@@ -62,9 +62,11 @@ __device__ __forceinline__ void ldv(const K* p, bool hint, uint64_t pol, K* x) {
 // probe's address plus an immediate.
 constexpr uint32_t kImgLoWords = 29056;   // 116224 B = half of sm_100's 227 KB opt-in
 
-template <class K>
+template <class K, bool PAIR>
 __device__ __forceinline__ bool img_less(const uint32_t* S, uint32_t w, K key) {
-    if constexpr (sizeof(K) == 8) {
+    if constexpr (PAIR) {
+        return reinterpret_cast<const uint64_t*>(S)[w] < (uint64_t)key;
+    } else if constexpr (sizeof(K) == 8) {
         const uint32_t qh = (uint32_t)((uint64_t)key >> 32);
         const uint32_t h = S[w];
         bool less = h < qh;
@@ -78,39 +80,40 @@ __device__ __forceinline__ bool img_less(const uint32_t* S, uint32_t w, K key) {
 // #{slots < key} of one shared-memory node (W sorted slots, MAX-padded past
 // K-1), by branch-free binary search over the image; `extra` = (K-1 == W)
 // adds the final compare that distinguishes "all W < key".
-template <class K, int W>
+template <class K, int W, bool PAIR>
 __device__ __forceinline__ uint32_t smem_node_rank(const uint32_t* S, uint32_t nd, K key, bool extra) {
     uint32_t c = 0;
 #pragma unroll
-    for (int s = W / 2; s >= 1; s >>= 1) c += img_less<K>(S, nd + c + s - 1, key) ? (uint32_t)s : 0u;
-    if (extra) c += img_less<K>(S, nd + c, key) ? 1u : 0u;
+    for (int s = W / 2; s >= 1; s >>= 1) c += img_less<K, PAIR>(S, nd + c + s - 1, key) ? (uint32_t)s : 0u;
+    if (extra) c += img_less<K, PAIR>(S, nd + c, key) ? 1u : 0u;
     return c;
 }
 
 // Stage the first `words` words of each image plane with TMA bulk copies:
 // hi (or the u32 plane) at word 0, lo at word kImgLoWords.
-template <class K>
+template <class K, bool PAIR>
 __device__ __forceinline__ void stage_image(uint32_t* S, const uint32_t* img, uint64_t plane_words, uint32_t words,
                                             uint64_t* bar) {
-    constexpr uint32_t planes = sizeof(K) == 8 ? 2 : 1;
+    constexpr uint32_t planes = (sizeof(K) == 8 && !PAIR) ? 2 : 1;
+    constexpr uint32_t unit = PAIR ? 8 : 4;
     if (threadIdx.x == 0) {
         mbar_init(bar, 1);
         fence_mbar_init();
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        mbar_arrive_expect_tx(bar, words * 4 * planes);
+        mbar_arrive_expect_tx(bar, words * unit * planes);
         constexpr uint32_t CH = 32768;
         for (uint32_t pl = 0; pl < planes; ++pl)
-            for (uint32_t o = 0; o < words * 4; o += CH) {
-                const uint32_t b = (words * 4 - o < CH) ? (words * 4 - o) : CH;
+            for (uint32_t o = 0; o < words * unit; o += CH) {
+                const uint32_t b = (words * unit - o < CH) ? (words * unit - o) : CH;
                 bulk_g2s((char*)(S + pl * kImgLoWords) + o, (const char*)(img + pl * plane_words) + o, b, bar);
             }
     }
     mbar_wait(bar, 0);
 }
 
-template <class K, int W, int R, int I>
+template <class K, int W, int R, int I, bool PAIR>
 __global__ void __launch_bounds__(1024, 1)
 k_kary_tiered(const KaryParams<K> p, const K* __restrict__ q, uint64_t m, void* __restrict__ out, uint32_t ob) {
     constexpr int V = (16 / (int)sizeof(K)) < W ? (16 / (int)sizeof(K)) : W;   // keys per lane per load
@@ -127,10 +130,8 @@ k_kary_tiered(const KaryParams<K> p, const K* __restrict__ q, uint64_t m, void* 
     const uint32_t j = lane % G;              // my lane within my group
     const uint32_t g = lane / G;              // my group within the warp
     const uint32_t gm = GMASK << (g * G);     // my group's lanes in a ballot
-    const uint32_t my_r = lane / GPW;         // wave that carries my own lookup
-    const uint32_t my_src = (lane % GPW) * G; // first lane of the group that carries it
 
-    if (p.img_words) stage_image<K>(S, p.img, p.img_plane_words, p.img_words, bar);
+    if (p.img_words) stage_image<K, PAIR>(S, p.img, p.img_plane_words, p.img_words, bar);
 
     const uint64_t pol_first = policy_evict_first();
     const uint64_t pol_last = policy_evict_last();
@@ -142,26 +143,32 @@ k_kary_tiered(const KaryParams<K> p, const K* __restrict__ q, uint64_t m, void* 
     const uint64_t nwt = (m + 31) / 32;
     uint64_t wt = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
 
-    K knext = KeyMax<K>::v;
-    if (wt < nwt && wt * 32 + lane < m) knext = load_stream(q + wt * 32 + lane, sh, pol_first);
+    // One shared-memory level of the thread-per-lookup descent.
+    auto smem_level = [&](uint32_t l, K key, uint32_t node) -> uint32_t {
+        const uint32_t c = smem_node_rank<K, W, PAIR>(S, p.img_base[l] + node * (W + 1), key, extra);
+        const uint32_t child = node * K_ + c;
+        const uint32_t last = p.nodes_next[l] - 1;
+        return child < last ? child : last;
+    };
+    auto load_tile = [&](uint64_t t) -> K {
+        const uint64_t i = t * 32 + lane;
+        return (t < nwt && i < m) ? load_stream(q + i, sh, pol_first) : KeyMax<K>::v;
+    };
+
+    // Software pipeline across warp-tiles: while the groups of this warp wait
+    // on the global-level and leaf loads of tile t, all 32 lanes advance the
+    // shared-memory descent of tile t+1 one level per load stage, so the
+    // shared-memory phase costs issue slots but no exposed latency.
+    // key/node: tile t (shared levels done); key_n/node_n: tile t+1 (descending);
+    // knext: the queries of tile t+2 (in flight).
+    K key = load_tile(wt);
+    uint32_t node = 0;
+    for (uint32_t l = 0; l < Ls; ++l) node = smem_level(l, key, node);
+    K key_n = load_tile(wt + warps_total);
+    K knext = load_tile(wt + 2 * warps_total);
 
     for (; wt < nwt; wt += warps_total) {
-        const K key = knext;
-        {
-            const uint64_t wn = wt + warps_total;
-            const uint64_t i = wn * 32 + lane;
-            knext = (wn < nwt && i < m) ? load_stream(q + i, sh, pol_first) : KeyMax<K>::v;
-        }
-        // ---- shared-memory levels: one thread per lookup, binary search in the node ----
-        uint32_t node = 0;
-        for (uint32_t l = 0; l < Ls; ++l) {
-            const uint32_t c = smem_node_rank<K, W>(S, p.img_base[l] + node * (W + 1), key, extra);
-            const uint32_t child = node * K_ + c;
-            const uint32_t last = p.nodes_next[l] - 1;
-            node = child < last ? child : last;
-        }
-        // ---- global levels + leaf: G lanes per lookup, I waves in flight ----
-        uint64_t mine = 0;
+        uint32_t node_n = 0, lvl_n = 0;
 #pragma unroll 1
         for (int b = 0; b < G / I; ++b) {
             K kk[I];
@@ -177,6 +184,7 @@ k_kary_tiered(const KaryParams<K> p, const K* __restrict__ q, uint64_t m, void* 
                 K s[I][V];
 #pragma unroll
                 for (int i = 0; i < I; ++i) ldv<K, V>(lv + (uint64_t)nn[i] * W, sep_last, pol_last, s[i]);
+                if (lvl_n < Ls) { node_n = smem_level(lvl_n, key_n, node_n); ++lvl_n; }
                 const uint32_t last = p.nodes_next[l] - 1;
 #pragma unroll
                 for (int i = 0; i < I; ++i) {
@@ -195,40 +203,49 @@ k_kary_tiered(const KaryParams<K> p, const K* __restrict__ q, uint64_t m, void* 
 #pragma unroll
                 for (int t = 0; t < R; ++t) ldv<K, V>(lp + t * V, lh, pol_first, &x[i][t * V]);
             }
+            if (lvl_n < Ls) { node_n = smem_level(lvl_n, key_n, node_n); ++lvl_n; }
 #pragma unroll
             for (int i = 0; i < I; ++i) {
-                const uint64_t p0 = (uint64_t)nn[i] * C + j * CPL;
+                // the MAX padding past n is never < q, so it never counts; it can
+                // equal q only when q == MAX, and then lb == n (a miss) — hence
+                // "hit" also requires lb < n and no per-key bounds test is needed
                 uint32_t lt = 0;
                 bool eq = false;
 #pragma unroll
                 for (int t = 0; t < CPL; ++t) {
-                    const bool ok = p0 + t < n;
-                    lt += (ok && x[i][t] < kk[i]) ? 1u : 0u;
-                    eq |= ok && x[i][t] == kk[i];
+                    lt += (x[i][t] < kk[i]) ? 1u : 0u;
+                    eq |= x[i][t] == kk[i];
                 }
 #pragma unroll
                 for (int o = G / 2; o > 0; o >>= 1) lt += __shfl_xor_sync(0xFFFFFFFFu, lt, o);
-                const bool hit = (__ballot_sync(0xFFFFFFFFu, eq) & gm) != 0;
-                uint64_t lbv = (uint64_t)nn[i] * C + lt;
-                if (lbv > n) lbv = n;
+                const uint64_t lbv = (uint64_t)nn[i] * C + lt;
+                const bool hit = ((__ballot_sync(0xFFFFFFFFu, eq) & gm) != 0) && lbv < n;
                 const uint64_t miss = ob == 8 ? (1ull << 63) : (1ull << 31);
                 const uint64_t res = hit ? lbv : (lbv | miss);
-                const uint64_t v = __shfl_sync(0xFFFFFFFFu, res, my_src);
-                if ((int)my_r == b * I + i) mine = v;
+                // the group's first lane stores; a wave's GPW results are contiguous
+                const uint64_t o = wt * 32 + (uint64_t)((b * I + i) * GPW) + g;
+                if (j == 0 && o < m) {
+                    if (ob == 8) store_stream((uint64_t*)out + o, res, sh, pol_first);
+                    else store_stream((uint32_t*)out + o, (uint32_t)res, sh, pol_first);
+                }
             }
         }
-        const uint64_t i = wt * 32 + lane;
-        if (i < m) {
-            if (ob == 8) store_stream((uint64_t*)out + i, mine, sh, pol_first);
-            else store_stream((uint32_t*)out + i, (uint32_t)mine, sh, pol_first);
-        }
+        // the rest of tile t+1's shared-memory levels (when they outnumber the load stages)
+        for (; lvl_n < Ls; ++lvl_n) node_n = smem_level(lvl_n, key_n, node_n);
+        key = key_n;
+        node = node_n;
+        key_n = knext;
+        knext = load_tile(wt + 3 * warps_total);
     }
 }
 
 template <class K, int W, int R, int I>
 static cudaError_t go_tiered(const void* params, const void* q, uint64_t m, void* out, uint32_t ob, uint32_t threads,
-                             Grid grid, uint32_t smem, cudaStream_t s, bool* uns) {
-    auto kern = k_kary_tiered<K, W, R, I>;
+                             bool pair64, Grid grid, uint32_t smem, cudaStream_t s, bool* uns) {
+    auto kern = k_kary_tiered<K, W, R, I, false>;
+    if constexpr (sizeof(K) == 8) {
+        if (pair64) kern = k_kary_tiered<K, W, R, I, true>;
+    }
     cudaFuncAttributes fa;
     cudaError_t e = cudaFuncGetAttributes(&fa, kern);
     if (e != cudaSuccess) return e;
@@ -257,16 +274,17 @@ static cudaError_t go_tiered(const void* params, const void* q, uint64_t m, void
 // W = node slots, R = C / W (1, 2, 4), I = waves in flight (clamped to a divisor of G)
 template <class K>
 cudaError_t dispatch_tiered(const void* params, const void* q, uint64_t m, void* out, uint32_t ob, uint32_t threads,
-                            uint32_t W, uint32_t R, uint32_t I, Grid grid, uint32_t smem, cudaStream_t s, bool* uns) {
+                            uint32_t W, uint32_t R, uint32_t I, bool pair64, Grid grid, uint32_t smem, cudaStream_t s,
+                            bool* uns) {
     constexpr int VK = 16 / (int)sizeof(K);
 #define BS_TI_I(WW, RR)                                                                                         \
     {                                                                                                           \
         constexpr int GG = WW / (VK < WW ? VK : WW);                                                            \
-        if (GG == 1 || I <= 1) return go_tiered<K, WW, RR, 1>(params, q, m, out, ob, threads, grid, smem, s, uns); \
+        if (GG == 1 || I <= 1) return go_tiered<K, WW, RR, 1>(params, q, m, out, ob, threads, pair64, grid, smem, s, uns); \
         if constexpr (GG >= 4) {                                                                                \
-            if (I >= 4) return go_tiered<K, WW, RR, 4>(params, q, m, out, ob, threads, grid, smem, s, uns);    \
+            if (I >= 4) return go_tiered<K, WW, RR, 4>(params, q, m, out, ob, threads, pair64, grid, smem, s, uns);    \
         }                                                                                                       \
-        if constexpr (GG >= 2) return go_tiered<K, WW, RR, 2>(params, q, m, out, ob, threads, grid, smem, s, uns); \
+        if constexpr (GG >= 2) return go_tiered<K, WW, RR, 2>(params, q, m, out, ob, threads, pair64, grid, smem, s, uns); \
     }
 #define BS_TI_R(WW)                          \
     case WW:                                 \

@@ -110,7 +110,8 @@ static int run_kary(const Index* ix, const void* q, uint64_t m, void* out, cudaS
         p.nodes_next[l] = (uint32_t)ix->k_next[l];
     }
     const uint32_t W = ix->kW, C = ix->kC;
-    const bool tiered = L.kary_mode == 2 && C >= W && (C / W == 1 || C / W == 2 || C / W == 4);
+    const bool tiered = L.kary_mode >= 2 && C >= W && (C / W == 1 || C / W == 2 || C / W == 4);
+    const bool pair64 = L.kary_mode == 3 && ix->kb == 8;
     const uint32_t threads = L.threads ? L.threads : (tiered ? 1024 : 512);
     const uint32_t R = L.nreg ? L.nreg : 2;
     const bool stat = L.schedule == BS_SCHED_STATIC;
@@ -133,26 +134,31 @@ static int run_kary(const Index* ix, const void* q, uint64_t m, void* out, cudaS
         // tiered: nreg = waves in flight (default 4, clamped to a divisor of the group size);
         // shared memory holds the image levels (odd node stride, hi/lo planes)
         const uint32_t I = L.nreg ? L.nreg : 4;
-        const uint32_t planes = ix->kb == 8 ? 2 : 1;
+        // pair64: one plane of 8-B slots; else u64: hi/lo 4-B planes, u32: one 4-B plane
+        const uint32_t planes = pair64 ? 1 : ix->kb == 8 ? 2 : 1;
+        const uint32_t unit = pair64 ? 8 : 4;
+        const uint32_t* base = pair64 ? ix->img64_base : ix->img_base;
+        const uint32_t imgL = pair64 ? ix->img64_L : ix->img_L;
+        const void* img = pair64 ? ix->d_img64 : ix->d_img;
         uint32_t Li = 0;
-        if (stat && L.use_pinned && ix->d_img) {
+        if (stat && L.use_pinned && img) {
             const uint64_t cap = smem_cap(ix, L.ctas_per_sm ? L.ctas_per_sm : 1) - 16;
-            const uint64_t budget = ix->layout.pin_bytes;   // image bytes (both planes)
-            auto need = [&](uint64_t w) { return planes == 2 ? (29056ull + w) * 4 : w * 4; };
-            while (Li < ix->img_L && need(ix->img_base[Li + 1]) <= cap &&
-                   (budget == 0xFFFFFFFFu || (uint64_t)ix->img_base[Li + 1] * 4 * planes <= budget))
+            const uint64_t budget = ix->layout.pin_bytes;   // image bytes (all planes)
+            auto need = [&](uint64_t w) { return planes == 2 ? (29056ull + w) * 4 : w * unit; };
+            while (Li < imgL && need(base[Li + 1]) <= cap &&
+                   (budget == 0xFFFFFFFFu || (uint64_t)base[Li + 1] * unit * planes <= budget))
                 ++Li;
         }
         p.Ls = Li;
-        p.img = (const uint32_t*)ix->d_img;
-        p.img_plane_words = ix->img_base[ix->img_L];
-        for (uint32_t l = 0; l < Li; ++l) p.img_base[l] = ix->img_base[l];
-        p.img_words = ix->img_base[Li];
-        // smem: [hi plane | pad to the lo offset | lo plane | mbarrier] (u32: [plane | mbarrier])
-        p.smem_bytes = (Li == 0 ? 0u : planes == 2 ? (29056u + p.img_words) * 4 : p.img_words * 4) + 16;
+        p.img = (const uint32_t*)img;
+        p.img_plane_words = base[imgL];
+        for (uint32_t l = 0; l < Li; ++l) p.img_base[l] = base[l];
+        p.img_words = base[Li];   // units: 4-B words (planes) or 8-B slots (pair64)
+        // smem: [hi plane | pad to the lo offset | lo plane | mbarrier] (u32 / pair64: [plane | mbarrier])
+        p.smem_bytes = (Li == 0 ? 0u : planes == 2 ? (29056u + p.img_words) * 4 : p.img_words * unit) + 16;
         const uint32_t tsmem = p.smem_bytes;
         ix->last_kary_smem = tsmem;
-        cudaError_t e = launch_kary_tiered(ix->kb, ix->ob, &p, q, m, out, threads, W, C / W, I, g, tsmem, s, &uns);
+        cudaError_t e = launch_kary_tiered(ix->kb, ix->ob, &p, q, m, out, threads, W, C / W, I, pair64, g, tsmem, s, &uns);
         if (uns) return fail(BS_ERR_UNSUPPORTED, "KARY tiered: threads=%u W=%u C=%u not supported", threads, W, C);
         if (e != cudaSuccess) return fail_cuda(e, "KARY tiered launch");
         return BS_OK;

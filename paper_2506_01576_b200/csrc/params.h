@@ -81,8 +81,8 @@ cudaError_t launch_kary_hybrid(int kb, int ob, const void* params, const void* q
 // 16-B vector loads by W*key/16 lanes per lookup below; R = C/W (1, 2, 4),
 // I = waves in flight; out word width ob passed at run time
 cudaError_t launch_kary_tiered(int kb, int ob, const void* params, const void* q, uint64_t m, void* out,
-                               uint32_t threads, uint32_t W, uint32_t R, uint32_t I, Grid grid, uint32_t smem,
-                               cudaStream_t s, bool* unsupported);
+                               uint32_t threads, uint32_t W, uint32_t R, uint32_t I, bool pair64, Grid grid,
+                               uint32_t smem, cudaStream_t s, bool* unsupported);
 
 // ---- build kernels ----
 cudaError_t build_check_sorted(int kb, const void* a, uint64_t n, int* d_flag, cudaStream_t s);
@@ -93,7 +93,7 @@ cudaError_t build_kary_levels(int kb, const void* a, uint64_t n, uint32_t K, uin
                               void* sep, uint64_t slots, cudaStream_t s);
 cudaError_t build_kary_image(int kb, const void* sep, uint32_t W, uint32_t L, const uint64_t* lvl_base,
                               const uint64_t* lvl_nodes, const uint32_t* img_base, uint64_t plane_words,
-                              void* img, cudaStream_t s);
+                              void* img, bool pair64, cudaStream_t s);
 cudaError_t build_sort_keys(int kb, const void* in, void* out, uint64_t n, cudaStream_t s);
 
 // ---- multi-GPU routing kernels (dist.cu) ----
