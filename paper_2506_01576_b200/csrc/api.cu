@@ -125,8 +125,10 @@ static int build_kary_layout(Index* ix, cudaStream_t st) {
     if (e != cudaSuccess) return fail_cuda(e, "build_kary_levels");
     // tiered shared-memory image: the longest level prefix whose planes fit one CTA's shared memory
     {
-        // u64: hi plane below word 29056 (kary_tiered.cuh kImgLoWords), lo plane above it
-        const uint64_t cap_words = kb == 8 ? ((uint64_t)ix->smem_optin - 1024 - 16) / 4 - 29056 : ((uint64_t)ix->smem_optin - 1024 - 16) / 4;
+        // levels whose hi-word plane alone fits one CTA's shared memory (kary_mode 6
+        // stages only that plane; modes 2/4 also need the lo plane at word 29056
+        // and take a shorter prefix at launch)
+        const uint64_t cap_words = ((uint64_t)ix->smem_optin - 1024 - 16) / 4;
         uint32_t words = 0, Li = 0;
         for (uint32_t l = 0; l < L; ++l) {
             const uint64_t w = ((ix->k_nodes[l] * (W + 1) + 3) / 4) * 4;   // 16-B multiple per level
@@ -224,7 +226,7 @@ int bs_build(const void* keys, uint64_t n, const bs_layout* layout_in, void** ou
     if (lay.variant > BS_VARIANT_KARY) return fail(BS_ERR_INVALID, "unknown variant %u", lay.variant);
     if (lay.schedule > BS_SCHED_STATIC) return fail(BS_ERR_INVALID, "unknown schedule %u", lay.schedule);
     if (lay.reorder > BS_REORDER_FULL) return fail(BS_ERR_INVALID, "unknown reorder %u", lay.reorder);
-    if (lay.kary_mode > 3) return fail(BS_ERR_INVALID, "unknown kary_mode %u", lay.kary_mode);
+    if (lay.kary_mode > 6) return fail(BS_ERR_INVALID, "unknown kary_mode %u", lay.kary_mode);
     if (lay.k < 2 || lay.k > 33) return fail(BS_ERR_INVALID, "K must be in [2, 33]");
     if (!is_pow2(lay.leaf_chunk) || lay.leaf_chunk > 256) return fail(BS_ERR_INVALID, "leaf_chunk must be a power of two <= 256");
     if (!reserved_zero(lay.reserved, 6)) return fail(BS_ERR_INVALID, "layout.reserved must be zero");
@@ -374,7 +376,7 @@ int bs_lookup_ex(const void* idx, const void* queries, uint64_t m, void* out, vo
     } else {
         bs_launch_default(idx, &L);
     }
-    if (L.kary_mode > 3) return fail(BS_ERR_INVALID, "bs_lookup: unknown kary_mode %u", L.kary_mode);
+    if (L.kary_mode > 6) return fail(BS_ERR_INVALID, "bs_lookup: unknown kary_mode %u", L.kary_mode);
     if (m == 0) return BS_OK;
     if (!queries || !out) return fail(BS_ERR_INVALID, "bs_lookup: NULL queries/out with m > 0");
     const uintptr_t q0 = (uintptr_t)queries, q1 = q0 + m * ix->kb;

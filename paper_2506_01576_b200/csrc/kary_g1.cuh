@@ -1,0 +1,255 @@
+// kary_g1.cuh — K-ary search (§5), "thread-per-lookup"
+// B200 schedule for small nodes (kary_mode 6).
+//
+// Same index and result as kary.cu.  Designed around the two limits the
+// tiered schedule (kary_tiered.cuh) runs into on B200 — issue slots and L1
+// data-pipe wavefronts:
+//
+//  * shared-memory levels: ONE thread per lookup, binary search inside each
+//    node over the image's hi-word plane only (u64; u32 keys are exact).  A
+//    hi-word tie sets a flag and the warp redoes those levels exactly from
+//    the global separator copy (rare for distinct keys, correct always).  With
+//    the lo plane out of shared memory, twice as many levels fit (227 KB).
+//  * global separator levels: still ONE thread per lookup — a node of
+//    W*key <= 64 B is one or two 256-bit loads (sm_100 LDG.E.ENL2.256) by the
+//    owning thread, so a level costs ~17 instructions per 32 lookups and no
+//    cross-lane traffic.  Small nodes (K = 5: 32 B, one sector) keep the L2
+//    traffic low; the extra levels are cheap because they are per thread.
+//  * leaf: GL = C*key/32 lanes per lookup, one 256-bit load each, so a 128-B
+//    leaf line is ONE wavefront; (key, chunk) arrive by __shfl_sync from the
+//    owner, the count is a packed full-warp REDUX (no wavefront), hit by
+//    __ballot_sync, and the group's last lane stores the result (a wave's
+//    32/GL results are contiguous).
+#pragma once
+#include "common.cuh"
+#include "kary_tiered.cuh"
+#include "params.h"
+
+namespace bs {
+
+// n x 32-B vector loads of a node / leaf piece (u64: 4 keys, u32: 8 keys per load)
+template <class K, int NV>
+__device__ __forceinline__ void ld_node(const K* p, bool hint, uint64_t pol, K* x) {
+    constexpr int V32 = 32 / (int)sizeof(K);
+    if constexpr (NV * (int)sizeof(K) <= 16) {
+        ldv<K, NV>(p, hint, pol, x);
+    } else {
+#pragma unroll
+        for (int t = 0; t < NV / V32; ++t) ldv<K, V32>(p + t * V32, hint, pol, x + t * V32);
+    }
+}
+
+template <class K, int W, int GL, int IL, int T>
+__global__ void __launch_bounds__(1024, 1)
+k_kary_g1(const KaryParams<K> p, const K* __restrict__ q, uint64_t m, void* __restrict__ out, uint32_t ob) {
+    constexpr int VL = 32 / (int)sizeof(K);     // leaf keys per lane (one 256-bit load)
+    constexpr int GPWL = 32 / GL;               // leaf lookups per wave
+    constexpr uint32_t GMASK = (GL == 32) ? 0xFFFFFFFFu : ((1u << GL) - 1u);
+    static_assert(GL >= 1 && 32 % GL == 0 && GL % IL == 0, "bad leaf shape");
+    static_assert(W * (int)sizeof(K) <= 64, "node of at most two 256-bit loads");
+
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint32_t* S = reinterpret_cast<uint32_t*>(smem);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + p.smem_bytes - 16);
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t jl = lane % GL;               // lane within its leaf group
+    const uint32_t gl = lane / GL;               // leaf group within the warp
+    const uint32_t gm = GMASK << (gl * GL);
+
+    if (p.img_words) stage_image<uint32_t, false>(S, p.img, p.img_plane_words, p.img_words, bar);
+
+    const uint64_t pol_first = policy_evict_first();
+    const uint64_t pol_last = policy_evict_last();
+    const bool sh = p.stream_hint != 0, lh = p.leaf_hint != 0, sep_last = p.sep_hint != 0;
+    const uint64_t n = p.n;
+    const uint32_t K_ = p.K, C = p.C, L = p.L, Ls = p.Ls;
+    const bool extra = (K_ - 1 == (uint32_t)W);
+    const uint32_t fb_leaf = bitlen_c(C - 1);
+    const uint64_t warps_total = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint64_t nwt = (m + 31) / 32;
+    uint64_t wt = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+
+    auto load_tile = [&](uint64_t t) -> K {
+        const uint64_t i = t * 32 + lane;
+        return (t < nwt && i < m) ? load_stream(q + i, sh, pol_first) : KeyMax<K>::v;
+    };
+    // exact in-node rank from the global separator copy (tie redo only)
+    auto node_rank_global = [&](uint32_t l, uint32_t node, K key) -> uint32_t {
+        const K* nd = p.sep + p.lvl_base[l] + (uint64_t)node * W;
+        uint32_t c = 0;
+#pragma unroll
+        for (int s = W / 2; s >= 1; s >>= 1) c += (ld_na(nd + c + s - 1) < key) ? (uint32_t)s : 0u;
+        if (extra) c += (ld_na(nd + c) < key) ? 1u : 0u;
+        return c;
+    };
+
+    // T warp-tiles per iteration: each thread carries T independent lookups
+    // through the shared and global levels (T loads in flight per thread)
+    const uint64_t wstep = warps_total * T;
+    wt = wt * T;
+    K key_n[T];
+#pragma unroll
+    for (int t = 0; t < T; ++t) key_n[t] = load_tile(wt + t);
+    for (; wt < nwt; wt += wstep) {
+        K key[T];
+#pragma unroll
+        for (int t = 0; t < T; ++t) {
+            key[t] = key_n[t];
+            key_n[t] = load_tile(wt + wstep + t);
+        }
+        // ---- shared-memory levels: hi words only, exact redo on a tie ----
+        uint32_t node[T];
+        bool tie = false;
+#pragma unroll
+        for (int t = 0; t < T; ++t) node[t] = 0;
+        for (uint32_t l = 0; l < Ls; ++l) {
+            const uint32_t last = p.nodes_next[l] - 1;
+            const uint32_t base = p.img_base[l];
+#pragma unroll
+            for (int t = 0; t < T; ++t) {
+                const uint32_t c = smem_node_rank<K, W, false, false>(S, base + node[t] * (W + 1), key[t], extra, tie);
+                const uint32_t child = node[t] * K_ + c;
+                node[t] = child < last ? child : last;
+            }
+        }
+        if (__any_sync(0xFFFFFFFFu, tie)) {
+#pragma unroll 1
+            for (int t = 0; t < T; ++t) {
+                node[t] = 0;
+                for (uint32_t l = 0; l < Ls; ++l) {
+                    const uint32_t child = node[t] * K_ + node_rank_global(l, node[t], key[t]);
+                    const uint32_t last = p.nodes_next[l] - 1;
+                    node[t] = child < last ? child : last;
+                }
+            }
+        }
+        // ---- global separator levels: thread per lookup, whole node in registers ----
+        for (uint32_t l = Ls; l < L; ++l) {
+            const K* lv = p.sep + p.lvl_base[l];
+            const uint32_t last = p.nodes_next[l] - 1;
+            K s[T][W];
+#pragma unroll
+            for (int t = 0; t < T; ++t) ld_node<K, W>(lv + (uint64_t)node[t] * W, sep_last, pol_last, s[t]);
+#pragma unroll
+            for (int t = 0; t < T; ++t) {
+                uint32_t c = 0;
+#pragma unroll
+                for (int v = 0; v < W; ++v) c += (s[t][v] < key[t]) ? 1u : 0u;
+                const uint32_t child = node[t] * K_ + c;
+                node[t] = child < last ? child : last;
+            }
+        }
+        // ---- leaf: GL lanes per lookup, IL waves in flight, T tiles ----
+#pragma unroll
+        for (int t = 0; t < T; ++t) {
+#pragma unroll 1
+        for (int b = 0; b < GL / IL; ++b) {
+            K kk[IL];
+            uint32_t cc[IL];
+            K x[IL][VL];
+#pragma unroll
+            for (int i = 0; i < IL; ++i) {
+                const int src = (b * IL + i) * GPWL + (int)gl;
+                kk[i] = __shfl_sync(0xFFFFFFFFu, key[t], src);
+                cc[i] = __shfl_sync(0xFFFFFFFFu, node[t], src);
+                ldv<K, VL>(p.a + (uint64_t)cc[i] * C + jl * VL, lh, pol_first, x[i]);
+            }
+#pragma unroll
+            for (int i = 0; i < IL; ++i) {
+                // MAX padding past n never counts and cannot make a hit (lb == n);
+                // the chunk's last key (last lane) is added back after the packed sum
+                uint32_t lt = 0;
+                bool eq = false;
+#pragma unroll
+                for (int u = 0; u < VL; ++u) {
+                    if (u < VL - 1 || jl != GL - 1) lt += (x[i][u] < kk[i]) ? 1u : 0u;
+                    eq |= x[i][u] == kk[i];
+                }
+                const bool last_lt = x[i][VL - 1] < kk[i];
+                lt = group_sum<GL>(lt, gl, fb_leaf);
+                const bool any_eq = (__ballot_sync(0xFFFFFFFFu, eq) & gm) != 0;
+                if (jl == GL - 1) {
+                    const uint64_t lbv = (uint64_t)cc[i] * C + lt + (last_lt ? 1u : 0u);
+                    const bool hit = any_eq && lbv < n;
+                    const uint64_t miss = ob == 8 ? (1ull << 63) : (1ull << 31);
+                    const uint64_t res = hit ? lbv : (lbv | miss);
+                    const uint64_t o = (wt + t) * 32 + (uint64_t)((b * IL + i) * GPWL) + gl;
+                    if (o < m) {
+                        if (ob == 8) store_stream((uint64_t*)out + o, res, sh, pol_first);
+                        else store_stream((uint32_t*)out + o, (uint32_t)res, sh, pol_first);
+                    }
+                }
+            }
+        }
+        }
+    }
+}
+
+template <class K, int W, int GL, int IL>
+static cudaError_t go_g1(const void* params, const void* q, uint64_t m, void* out, uint32_t ob, uint32_t threads,
+                         uint32_t T, Grid grid, uint32_t smem, cudaStream_t s, bool* uns) {
+    auto kern = T >= 2 ? k_kary_g1<K, W, GL, IL, 2> : k_kary_g1<K, W, GL, IL, 1>;
+    cudaFuncAttributes fa;
+    cudaError_t e = cudaFuncGetAttributes(&fa, kern);
+    if (e != cudaSuccess) return e;
+    if ((int)threads > fa.maxThreadsPerBlock || threads % 32) { *uns = true; return cudaSuccess; }
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const uint64_t need = (m + threads - 1) / threads;
+    uint64_t g = need;
+    if (grid.sched_static) {
+        int occ = (int)grid.ctas_per_sm;
+        if (occ == 0) {
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, (int)threads, smem);
+            if (e != cudaSuccess) return e;
+        }
+        if (occ < 1) { *uns = true; return cudaSuccess; }
+        g = (uint64_t)grid.sm_count * (uint64_t)occ;
+    }
+    if (g > need) g = need;
+    if (g == 0) g = 1;
+    if (g > 0x7FFFFFFFull) g = 0x7FFFFFFFull;
+    kern<<<(unsigned)g, threads, smem, s>>>(*(const KaryParams<K>*)params, (const K*)q, m, out, ob);
+    return cudaGetLastError();
+}
+
+// W = node slots (W*key <= 64 B), GL = leaf lanes (C*key = 32*GL), IL = leaf waves in flight
+template <class K>
+cudaError_t dispatch_g1(const void* params, const void* q, uint64_t m, void* out, uint32_t ob, uint32_t threads,
+                        uint32_t W, uint32_t GL, uint32_t IL, uint32_t T, Grid grid, uint32_t smem, cudaStream_t s,
+                        bool* uns) {
+#define BS_G1_IL(WW, GG)                                                                                  \
+    {                                                                                                     \
+        if (IL >= 4 && GG >= 4) return go_g1<K, WW, GG, (GG >= 4 ? 4 : 1)>(params, q, m, out, ob, threads, T, grid, smem, s, uns); \
+        if (IL >= 2 && GG >= 2) return go_g1<K, WW, GG, (GG >= 2 ? 2 : 1)>(params, q, m, out, ob, threads, T, grid, smem, s, uns); \
+        return go_g1<K, WW, GG, 1>(params, q, m, out, ob, threads, T, grid, smem, s, uns);                  \
+    }
+#define BS_G1_G(WW)                             \
+    case WW:                                    \
+        if (GL == 1) BS_G1_IL(WW, 1)            \
+        if (GL == 2) BS_G1_IL(WW, 2)            \
+        if (GL == 4) BS_G1_IL(WW, 4)            \
+        if (GL == 8) BS_G1_IL(WW, 8)            \
+        break;
+    constexpr int WMAX = 64 / (int)sizeof(K);
+    switch (W) {
+        BS_G1_G(2)
+        BS_G1_G(4)
+        BS_G1_G(8)
+        case 16:
+            if constexpr (WMAX >= 16) {
+                if (GL == 1) BS_G1_IL(16, 1)
+                if (GL == 2) BS_G1_IL(16, 2)
+                if (GL == 4) BS_G1_IL(16, 4)
+                if (GL == 8) BS_G1_IL(16, 8)
+            }
+            break;
+        default: break;
+    }
+#undef BS_G1_G
+#undef BS_G1_IL
+    *uns = true;
+    return cudaSuccess;
+}
+
+}  // namespace bs

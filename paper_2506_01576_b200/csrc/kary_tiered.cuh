@@ -11,28 +11,46 @@
 //    (log2(W) dependent 8-B shared loads, +1 when K-1 == W) instead of reading
 //    all W slots — a node is sorted, so this is the same count of separators
 //    < q at a quarter of the shared-memory wavefronts.
-//  * global levels + leaf (L2 / HBM): G = W*key/16 lanes per lookup, each lane
-//    one 16-B vector load, so a node is ONE coalesced request of W*key bytes
+//  * global levels + leaf (L2 / HBM): G = W*key/32 lanes per lookup, each lane
+//    one 32-B vector load (sm_100 256-bit LDG), so a node is ONE coalesced request of W*key bytes
 //    ("K-1 threads compare in parallel"; on B200 one 128-B line for
-//    K = 17 u64).  The group counts separators < q with one __ballot_sync per
-//    vector element and __popc.  A warp's 32 lookups are handed to its 32/G
+//    K = 17 u64).  The group counts separators < q per lane and sums the
+//    counts over its lanes with packed full-warp REDUX adds (group_sum).  A warp's 32 lookups are handed to its 32/G
 //    groups in G waves (__shfl_sync), I waves in flight at a time.
-//  * leaf: CPL = C/G keys per lane (R = C/W vector loads of 16 B); positions
+//  * leaf: CPL = C/G keys per lane (R = C/W vector loads of 32 B); positions
 //    >= n read the MAX padding that bs_build writes and are masked out.
-//  * each group's first lane stores its result (a wave's 32/G results are
+//  * the group's last lane stores the result (a wave's 32/G results are
 //    contiguous); the next warp-tile's queries are prefetched during the descent.
+//  * PIPE: software pipeline across warp-tiles — the shared-memory descent of
+//    tile t+1 is interleaved with the load stages of tile t.
 #pragma once
 #include "common.cuh"
 #include "params.h"
 
 namespace bs {
 
-// V keys (V*sizeof(K) in {8, 16} bytes) from global memory, no L1 allocation,
+// V keys (V*sizeof(K) in {8, 16, 32} bytes) from global memory, no L1 allocation,
 // optional L2 eviction-priority policy.
 template <class K, int V>
 __device__ __forceinline__ void ldv(const K* p, bool hint, uint64_t pol, K* x) {
-    if constexpr (sizeof(K) == 8) {
-        static_assert(V == 2, "u64: 16-B vectors");
+    if constexpr (sizeof(K) == 8 && V == 4) {   // 256-bit load (sm_100: LDG.E.ENL2.256)
+        if (hint)
+            asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u64 {%0,%1,%2,%3}, [%4], %5;"
+                         : "=l"(x[0]), "=l"(x[1]), "=l"(x[2]), "=l"(x[3]) : "l"(p), "l"(pol));
+        else
+            asm volatile("ld.global.nc.L1::no_allocate.v4.u64 {%0,%1,%2,%3}, [%4];"
+                         : "=l"(x[0]), "=l"(x[1]), "=l"(x[2]), "=l"(x[3]) : "l"(p));
+    } else if constexpr (sizeof(K) == 4 && V == 8) {
+        if (hint)
+            asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+                         : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]), "=r"(x[4]), "=r"(x[5]), "=r"(x[6]), "=r"(x[7])
+                         : "l"(p), "l"(pol));
+        else
+            asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                         : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]), "=r"(x[4]), "=r"(x[5]), "=r"(x[6]), "=r"(x[7])
+                         : "l"(p));
+    } else if constexpr (sizeof(K) == 8) {
+        static_assert(V == 2, "u64: 16- or 32-B vectors");
         if (hint)
             asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u64 {%0,%1}, [%2], %3;"
                          : "=l"(x[0]), "=l"(x[1]) : "l"(p), "l"(pol));
@@ -46,7 +64,7 @@ __device__ __forceinline__ void ldv(const K* p, bool hint, uint64_t pol, K* x) {
             asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
                          : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]) : "l"(p));
     } else {
-        static_assert(V == 2, "u32: 8- or 16-B vectors");
+        static_assert(V == 2, "u32: 8-, 16- or 32-B vectors");
         if (hint)
             asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;"
                          : "=r"(x[0]), "=r"(x[1]) : "l"(p), "l"(pol));
@@ -62,16 +80,26 @@ __device__ __forceinline__ void ldv(const K* p, bool hint, uint64_t pol, K* x) {
 // probe's address plus an immediate.
 constexpr uint32_t kImgLoWords = 29056;   // 116224 B = half of sm_100's 227 KB opt-in
 
-template <class K, bool PAIR>
-__device__ __forceinline__ bool img_less(const uint32_t* S, uint32_t w, K key) {
+// slot < key for a slot of the shared-memory image.  EXACT: u32 keys read the
+// one plane, PAIR reads the 8-B slot, u64 reads the hi word and then the lo
+// word.  !EXACT (u64, planes): the hi word alone decides and `tie` records a
+// hi-word tie, in which case the caller redoes the descent exactly — a
+// predicated-off shared load still costs an L1 wavefront
+// (tools/ubench_shfl.cu), so the lo plane must not be touched in the common
+// case.
+template <class K, bool PAIR, bool EXACT>
+__device__ __forceinline__ bool img_less(const uint32_t* S, uint32_t w, K key, bool& tie) {
     if constexpr (PAIR) {
         return reinterpret_cast<const uint64_t*>(S)[w] < (uint64_t)key;
     } else if constexpr (sizeof(K) == 8) {
         const uint32_t qh = (uint32_t)((uint64_t)key >> 32);
         const uint32_t h = S[w];
-        bool less = h < qh;
-        if (h == qh) less = S[kImgLoWords + w] < (uint32_t)key;
-        return less;
+        if constexpr (EXACT) {
+            return h < qh || (h == qh && S[kImgLoWords + w] < (uint32_t)key);
+        } else {
+            tie |= h == qh;
+            return h < qh;
+        }
     } else {
         return S[w] < (uint32_t)key;
     }
@@ -80,14 +108,37 @@ __device__ __forceinline__ bool img_less(const uint32_t* S, uint32_t w, K key) {
 // #{slots < key} of one shared-memory node (W sorted slots, MAX-padded past
 // K-1), by branch-free binary search over the image; `extra` = (K-1 == W)
 // adds the final compare that distinguishes "all W < key".
-template <class K, int W, bool PAIR>
-__device__ __forceinline__ uint32_t smem_node_rank(const uint32_t* S, uint32_t nd, K key, bool extra) {
+template <class K, int W, bool PAIR, bool EXACT>
+__device__ __forceinline__ uint32_t smem_node_rank(const uint32_t* S, uint32_t nd, K key, bool extra, bool& tie) {
     uint32_t c = 0;
 #pragma unroll
-    for (int s = W / 2; s >= 1; s >>= 1) c += img_less<K, PAIR>(S, nd + c + s - 1, key) ? (uint32_t)s : 0u;
-    if (extra) c += img_less<K, PAIR>(S, nd + c, key) ? 1u : 0u;
+    for (int s = W / 2; s >= 1; s >>= 1) c += img_less<K, PAIR, EXACT>(S, nd + c + s - 1, key, tie) ? (uint32_t)s : 0u;
+    if (extra) c += img_less<K, PAIR, EXACT>(S, nd + c, key, tie) ? 1u : 0u;
     return c;
 }
+
+// Per-group sum of per-lane counts c (every group's sum < 2^fb).  When the
+// warp's groups fit one 32-bit word of fb-bit fields, each lane adds
+// c << (fb*g) into one full-warp REDUX.SUM (no L1 wavefront) and extracts its
+// field; otherwise a __shfl_xor_sync butterfly (one wavefront per step).
+template <int G>
+__device__ __forceinline__ uint32_t group_sum(uint32_t c, uint32_t g, uint32_t fb) {
+    if constexpr (G == 1) {
+        return c;
+    } else {
+        constexpr uint32_t GPW = 32 / G;
+        if (GPW * fb <= 32) {
+            const uint32_t sh = g * fb;
+            const uint32_t tot = __reduce_add_sync(0xFFFFFFFFu, c << sh);
+            return (tot >> sh) & ((1u << fb) - 1u);
+        }
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+        return c;
+    }
+}
+
+constexpr uint32_t bitlen_c(uint32_t x) { return x == 0 ? 0 : 1 + bitlen_c(x >> 1); }
 
 // Stage the first `words` words of each image plane with TMA bulk copies:
 // hi (or the u32 plane) at word 0, lo at word kImgLoWords.
@@ -113,10 +164,10 @@ __device__ __forceinline__ void stage_image(uint32_t* S, const uint32_t* img, ui
     mbar_wait(bar, 0);
 }
 
-template <class K, int W, int R, int I, bool PAIR>
+template <class K, int W, int R, int I, bool PAIR, bool PIPE>
 __global__ void __launch_bounds__(1024, 1)
 k_kary_tiered(const KaryParams<K> p, const K* __restrict__ q, uint64_t m, void* __restrict__ out, uint32_t ob) {
-    constexpr int V = (16 / (int)sizeof(K)) < W ? (16 / (int)sizeof(K)) : W;   // keys per lane per load
+    constexpr int V = (32 / (int)sizeof(K)) < W ? (32 / (int)sizeof(K)) : W;   // keys per lane per load (<= 32 B)
     constexpr int G = W / V;                                                  // lanes per lookup
     constexpr int GPW = 32 / G;                                               // lookups per wave
     constexpr int CPL = R * V;                                                // leaf keys per lane
@@ -139,16 +190,34 @@ k_kary_tiered(const KaryParams<K> p, const K* __restrict__ q, uint64_t m, void* 
     const uint64_t n = p.n;
     const uint32_t K_ = p.K, C = p.C, L = p.L, Ls = p.Ls;
     const bool extra = (K_ - 1 == (uint32_t)W);
+    // field widths for the packed group sums: a node count is <= min(K-1, W);
+    // a leaf count without the chunk's last key is <= C-1
+    const uint32_t fb_node = bitlen_c(K_ - 1 < (uint32_t)W ? K_ - 1 : (uint32_t)W);
+    const uint32_t fb_leaf = bitlen_c(C - 1);
     const uint64_t warps_total = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     const uint64_t nwt = (m + 31) / 32;
     uint64_t wt = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
 
-    // One shared-memory level of the thread-per-lookup descent.
-    auto smem_level = [&](uint32_t l, K key, uint32_t node) -> uint32_t {
-        const uint32_t c = smem_node_rank<K, W, PAIR>(S, p.img_base[l] + node * (W + 1), key, extra);
+    // One shared-memory level of the thread-per-lookup descent (hi words only
+    // for u64 planes; `tie` set when a hi word tied), and the exact descent
+    // the warp redoes when any lane tied (rare for distinct keys, always for
+    // keys that share their hi words — correct either way).
+    auto smem_level = [&](uint32_t l, K key, uint32_t node, bool& tie) -> uint32_t {
+        const uint32_t c = smem_node_rank<K, W, PAIR, false>(S, p.img_base[l] + node * (W + 1), key, extra, tie);
         const uint32_t child = node * K_ + c;
         const uint32_t last = p.nodes_next[l] - 1;
         return child < last ? child : last;
+    };
+    auto smem_exact = [&](K key) -> uint32_t {
+        uint32_t node = 0;
+        bool unused = false;
+        for (uint32_t l = 0; l < Ls; ++l) {
+            const uint32_t c = smem_node_rank<K, W, PAIR, true>(S, p.img_base[l] + node * (W + 1), key, extra, unused);
+            const uint32_t child = node * K_ + c;
+            const uint32_t last = p.nodes_next[l] - 1;
+            node = child < last ? child : last;
+        }
+        return node;
     };
     auto load_tile = [&](uint64_t t) -> K {
         const uint64_t i = t * 32 + lane;
@@ -163,12 +232,23 @@ k_kary_tiered(const KaryParams<K> p, const K* __restrict__ q, uint64_t m, void* 
     // knext: the queries of tile t+2 (in flight).
     K key = load_tile(wt);
     uint32_t node = 0;
-    for (uint32_t l = 0; l < Ls; ++l) node = smem_level(l, key, node);
+    if (PIPE) {
+        bool tie = false;
+        for (uint32_t l = 0; l < Ls; ++l) node = smem_level(l, key, node, tie);
+        if (__any_sync(0xFFFFFFFFu, tie)) node = smem_exact(key);
+    }
     K key_n = load_tile(wt + warps_total);
-    K knext = load_tile(wt + 2 * warps_total);
+    K knext = PIPE ? load_tile(wt + 2 * warps_total) : KeyMax<K>::v;
 
     for (; wt < nwt; wt += warps_total) {
-        uint32_t node_n = 0, lvl_n = 0;
+        if (!PIPE) {   // shared-memory descent of this tile, then its global phase
+            node = 0;
+            bool tie = false;
+            for (uint32_t l = 0; l < Ls; ++l) node = smem_level(l, key, node, tie);
+            if (__any_sync(0xFFFFFFFFu, tie)) node = smem_exact(key);
+        }
+        uint32_t node_n = 0, lvl_n = PIPE ? 0 : Ls;
+        bool tie_n = false;
 #pragma unroll 1
         for (int b = 0; b < G / I; ++b) {
             K kk[I];
@@ -184,13 +264,14 @@ k_kary_tiered(const KaryParams<K> p, const K* __restrict__ q, uint64_t m, void* 
                 K s[I][V];
 #pragma unroll
                 for (int i = 0; i < I; ++i) ldv<K, V>(lv + (uint64_t)nn[i] * W, sep_last, pol_last, s[i]);
-                if (lvl_n < Ls) { node_n = smem_level(lvl_n, key_n, node_n); ++lvl_n; }
+                if (PIPE && lvl_n < Ls) { node_n = smem_level(lvl_n, key_n, node_n, tie_n); ++lvl_n; }
                 const uint32_t last = p.nodes_next[l] - 1;
 #pragma unroll
                 for (int i = 0; i < I; ++i) {
                     uint32_t c = 0;
 #pragma unroll
-                    for (int v = 0; v < V; ++v) c += __popc(__ballot_sync(0xFFFFFFFFu, s[i][v] < kk[i]) & gm);
+                    for (int v = 0; v < V; ++v) c += (s[i][v] < kk[i]) ? 1u : 0u;
+                    c = group_sum<G>(c, g, fb_node);
                     const uint32_t child = nn[i] * K_ + c;
                     nn[i] = child < last ? child : last;
                 }
@@ -203,48 +284,61 @@ k_kary_tiered(const KaryParams<K> p, const K* __restrict__ q, uint64_t m, void* 
 #pragma unroll
                 for (int t = 0; t < R; ++t) ldv<K, V>(lp + t * V, lh, pol_first, &x[i][t * V]);
             }
-            if (lvl_n < Ls) { node_n = smem_level(lvl_n, key_n, node_n); ++lvl_n; }
+            if (PIPE && lvl_n < Ls) { node_n = smem_level(lvl_n, key_n, node_n, tie_n); ++lvl_n; }
 #pragma unroll
             for (int i = 0; i < I; ++i) {
                 // the MAX padding past n is never < q, so it never counts; it can
                 // equal q only when q == MAX, and then lb == n (a miss) — hence
                 // "hit" also requires lb < n and no per-key bounds test is needed
+                // the group's last lane holds the chunk's last key; it is left
+                // out of the packed sum (< C = 2^(fb_leaf) - 1 + 1) and added
+                // back by that lane, which also stores the result
                 uint32_t lt = 0;
                 bool eq = false;
 #pragma unroll
                 for (int t = 0; t < CPL; ++t) {
-                    lt += (x[i][t] < kk[i]) ? 1u : 0u;
+                    const bool lt_t = x[i][t] < kk[i];
+                    if (t < CPL - 1 || j != G - 1) lt += lt_t ? 1u : 0u;
                     eq |= x[i][t] == kk[i];
                 }
-#pragma unroll
-                for (int o = G / 2; o > 0; o >>= 1) lt += __shfl_xor_sync(0xFFFFFFFFu, lt, o);
-                const uint64_t lbv = (uint64_t)nn[i] * C + lt;
-                const bool hit = ((__ballot_sync(0xFFFFFFFFu, eq) & gm) != 0) && lbv < n;
-                const uint64_t miss = ob == 8 ? (1ull << 63) : (1ull << 31);
-                const uint64_t res = hit ? lbv : (lbv | miss);
-                // the group's first lane stores; a wave's GPW results are contiguous
-                const uint64_t o = wt * 32 + (uint64_t)((b * I + i) * GPW) + g;
-                if (j == 0 && o < m) {
-                    if (ob == 8) store_stream((uint64_t*)out + o, res, sh, pol_first);
-                    else store_stream((uint32_t*)out + o, (uint32_t)res, sh, pol_first);
+                const bool last_lt = x[i][CPL - 1] < kk[i];
+                lt = group_sum<G>(lt, g, fb_leaf);
+                const bool any_eq = (__ballot_sync(0xFFFFFFFFu, eq) & gm) != 0;
+                if (j == G - 1) {
+                    const uint64_t lbv = (uint64_t)nn[i] * C + lt + (last_lt ? 1u : 0u);
+                    const bool hit = any_eq && lbv < n;
+                    const uint64_t miss = ob == 8 ? (1ull << 63) : (1ull << 31);
+                    const uint64_t res = hit ? lbv : (lbv | miss);
+                    // a wave's GPW results are contiguous: one store instruction per wave
+                    const uint64_t o = wt * 32 + (uint64_t)((b * I + i) * GPW) + g;
+                    if (o < m) {
+                        if (ob == 8) store_stream((uint64_t*)out + o, res, sh, pol_first);
+                        else store_stream((uint32_t*)out + o, (uint32_t)res, sh, pol_first);
+                    }
                 }
             }
         }
-        // the rest of tile t+1's shared-memory levels (when they outnumber the load stages)
-        for (; lvl_n < Ls; ++lvl_n) node_n = smem_level(lvl_n, key_n, node_n);
-        key = key_n;
-        node = node_n;
-        key_n = knext;
-        knext = load_tile(wt + 3 * warps_total);
+        if (PIPE) {
+            // the rest of tile t+1's shared-memory levels (when they outnumber the load stages)
+            for (; lvl_n < Ls; ++lvl_n) node_n = smem_level(lvl_n, key_n, node_n, tie_n);
+            if (__any_sync(0xFFFFFFFFu, tie_n)) node_n = smem_exact(key_n);
+            key = key_n;
+            node = node_n;
+            key_n = knext;
+            knext = load_tile(wt + 3 * warps_total);
+        } else {
+            key = key_n;
+            key_n = load_tile(wt + 2 * warps_total);
+        }
     }
 }
 
 template <class K, int W, int R, int I>
 static cudaError_t go_tiered(const void* params, const void* q, uint64_t m, void* out, uint32_t ob, uint32_t threads,
-                             bool pair64, Grid grid, uint32_t smem, cudaStream_t s, bool* uns) {
-    auto kern = k_kary_tiered<K, W, R, I, false>;
+                             bool pair64, bool pipe, Grid grid, uint32_t smem, cudaStream_t s, bool* uns) {
+    auto kern = pipe ? k_kary_tiered<K, W, R, I, false, true> : k_kary_tiered<K, W, R, I, false, false>;
     if constexpr (sizeof(K) == 8) {
-        if (pair64) kern = k_kary_tiered<K, W, R, I, true>;
+        if (pair64) kern = pipe ? k_kary_tiered<K, W, R, I, true, true> : k_kary_tiered<K, W, R, I, true, false>;
     }
     cudaFuncAttributes fa;
     cudaError_t e = cudaFuncGetAttributes(&fa, kern);
@@ -274,17 +368,17 @@ static cudaError_t go_tiered(const void* params, const void* q, uint64_t m, void
 // W = node slots, R = C / W (1, 2, 4), I = waves in flight (clamped to a divisor of G)
 template <class K>
 cudaError_t dispatch_tiered(const void* params, const void* q, uint64_t m, void* out, uint32_t ob, uint32_t threads,
-                            uint32_t W, uint32_t R, uint32_t I, bool pair64, Grid grid, uint32_t smem, cudaStream_t s,
-                            bool* uns) {
-    constexpr int VK = 16 / (int)sizeof(K);
+                            uint32_t W, uint32_t R, uint32_t I, bool pair64, bool pipe, Grid grid, uint32_t smem,
+                            cudaStream_t s, bool* uns) {
+    constexpr int VK = 32 / (int)sizeof(K);
 #define BS_TI_I(WW, RR)                                                                                         \
     {                                                                                                           \
         constexpr int GG = WW / (VK < WW ? VK : WW);                                                            \
-        if (GG == 1 || I <= 1) return go_tiered<K, WW, RR, 1>(params, q, m, out, ob, threads, pair64, grid, smem, s, uns); \
+        if (GG == 1 || I <= 1) return go_tiered<K, WW, RR, 1>(params, q, m, out, ob, threads, pair64, pipe, grid, smem, s, uns); \
         if constexpr (GG >= 4) {                                                                                \
-            if (I >= 4) return go_tiered<K, WW, RR, 4>(params, q, m, out, ob, threads, pair64, grid, smem, s, uns);    \
+            if (I >= 4) return go_tiered<K, WW, RR, 4>(params, q, m, out, ob, threads, pair64, pipe, grid, smem, s, uns);    \
         }                                                                                                       \
-        if constexpr (GG >= 2) return go_tiered<K, WW, RR, 2>(params, q, m, out, ob, threads, pair64, grid, smem, s, uns); \
+        if constexpr (GG >= 2) return go_tiered<K, WW, RR, 2>(params, q, m, out, ob, threads, pair64, pipe, grid, smem, s, uns); \
     }
 #define BS_TI_R(WW)                          \
     case WW:                                 \

@@ -110,9 +110,13 @@ static int run_kary(const Index* ix, const void* q, uint64_t m, void* out, cudaS
         p.nodes_next[l] = (uint32_t)ix->k_next[l];
     }
     const uint32_t W = ix->kW, C = ix->kC;
-    const bool tiered = L.kary_mode >= 2 && C >= W && (C / W == 1 || C / W == 2 || C / W == 4);
-    const bool pair64 = L.kary_mode == 3 && ix->kb == 8;
-    const uint32_t threads = L.threads ? L.threads : (tiered ? 1024 : 512);
+    const uint32_t GL = C * ix->kb / 32;
+    const bool g1 = L.kary_mode == 6 && W * ix->kb <= 64 && W * ix->kb >= 8 && C * ix->kb >= 32 &&
+                    C * ix->kb <= 256;
+    const bool tiered = !g1 && L.kary_mode >= 2 && C >= W && (C / W == 1 || C / W == 2 || C / W == 4);
+    const bool pair64 = (L.kary_mode == 3 || L.kary_mode == 5) && ix->kb == 8;
+    const bool pipe = L.kary_mode >= 4;   // 4/5: experimental software-pipelined 2/3
+    const uint32_t threads = L.threads ? L.threads : ((tiered || g1) ? 1024 : 512);
     const uint32_t R = L.nreg ? L.nreg : 2;
     const bool stat = L.schedule == BS_SCHED_STATIC;
     uint32_t Ls = 0, sbytes = 0;
@@ -130,6 +134,32 @@ static int run_kary(const Index* ix, const void* q, uint64_t m, void* out, cudaS
     bool uns = false;
     Grid g{stat ? 1u : 0u, L.ctas_per_sm, (uint32_t)ix->sm_count};
     const uint32_t cpl = C >= W ? C / W : 1;
+    if (g1) {
+        // hi-word plane of the image only (u64), or the u32 plane
+        uint32_t Li = 0;
+        if (stat && L.use_pinned && ix->d_img) {
+            const uint64_t cap = smem_cap(ix, L.ctas_per_sm ? L.ctas_per_sm : 1) - 16;
+            const uint64_t budget = ix->layout.pin_bytes;
+            while (Li < ix->img_L && (uint64_t)ix->img_base[Li + 1] * 4 <= cap &&
+                   (budget == 0xFFFFFFFFu || (uint64_t)ix->img_base[Li + 1] * 4 <= budget))
+                ++Li;
+        }
+        p.Ls = Li;
+        p.img = (const uint32_t*)ix->d_img;
+        p.img_plane_words = ix->img_base[ix->img_L];
+        for (uint32_t l = 0; l < Li; ++l) p.img_base[l] = ix->img_base[l];
+        p.img_words = ix->img_base[Li];
+        p.smem_bytes = p.img_words * 4 + 16;
+        ix->last_kary_smem = p.smem_bytes;
+        // nreg: low 4 bits = leaf waves in flight IL (default 4), bits 4.. = lookups
+        // per thread T (1 or 2, default 1)
+        const uint32_t IL = (L.nreg & 15) ? (L.nreg & 15) : 4;
+        const uint32_t T = (L.nreg >> 4) ? (L.nreg >> 4) : 1;
+        cudaError_t e = launch_kary_g1(ix->kb, ix->ob, &p, q, m, out, threads, W, GL, IL, T, g, p.smem_bytes, s, &uns);
+        if (uns) return fail(BS_ERR_UNSUPPORTED, "KARY g1: threads=%u W=%u C=%u not supported", threads, W, C);
+        if (e != cudaSuccess) return fail_cuda(e, "KARY g1 launch");
+        return BS_OK;
+    }
     if (tiered) {
         // tiered: nreg = waves in flight (default 4, clamped to a divisor of the group size);
         // shared memory holds the image levels (odd node stride, hi/lo planes)
@@ -158,7 +188,7 @@ static int run_kary(const Index* ix, const void* q, uint64_t m, void* out, cudaS
         p.smem_bytes = (Li == 0 ? 0u : planes == 2 ? (29056u + p.img_words) * 4 : p.img_words * unit) + 16;
         const uint32_t tsmem = p.smem_bytes;
         ix->last_kary_smem = tsmem;
-        cudaError_t e = launch_kary_tiered(ix->kb, ix->ob, &p, q, m, out, threads, W, C / W, I, pair64, g, tsmem, s, &uns);
+        cudaError_t e = launch_kary_tiered(ix->kb, ix->ob, &p, q, m, out, threads, W, C / W, I, pair64, pipe, g, tsmem, s, &uns);
         if (uns) return fail(BS_ERR_UNSUPPORTED, "KARY tiered: threads=%u W=%u C=%u not supported", threads, W, C);
         if (e != cudaSuccess) return fail_cuda(e, "KARY tiered launch");
         return BS_OK;

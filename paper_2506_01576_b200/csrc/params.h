@@ -81,8 +81,14 @@ cudaError_t launch_kary_hybrid(int kb, int ob, const void* params, const void* q
 // 16-B vector loads by W*key/16 lanes per lookup below; R = C/W (1, 2, 4),
 // I = waves in flight; out word width ob passed at run time
 cudaError_t launch_kary_tiered(int kb, int ob, const void* params, const void* q, uint64_t m, void* out,
-                               uint32_t threads, uint32_t W, uint32_t R, uint32_t I, bool pair64, Grid grid,
-                               uint32_t smem, cudaStream_t s, bool* unsupported);
+                               uint32_t threads, uint32_t W, uint32_t R, uint32_t I, bool pair64, bool pipe,
+                               Grid grid, uint32_t smem, cudaStream_t s, bool* unsupported);
+
+// thread-per-lookup K-ary (kary_g1.cuh, kary_mode 6): W*key <= 64 B nodes,
+// GL = C*key/32 leaf lanes, IL leaf waves in flight, T lookups per thread in flight
+cudaError_t launch_kary_g1(int kb, int ob, const void* params, const void* q, uint64_t m, void* out,
+                           uint32_t threads, uint32_t W, uint32_t GL, uint32_t IL, uint32_t T, Grid grid,
+                           uint32_t smem, cudaStream_t s, bool* unsupported);
 
 // ---- build kernels ----
 cudaError_t build_check_sorted(int kb, const void* a, uint64_t n, int* d_flag, cudaStream_t s);
