@@ -186,7 +186,7 @@ def main():
     ap.add_argument("--reorder", type=int, default=0)
     ap.add_argument("--schedule", type=int, default=1)
     ap.add_argument("--hints", type=int, default=3)
-    ap.add_argument("--kary-mode", type=int, default=2, help="0 warp, 1 hybrid, 2 tiered, 3 tiered 8-B probes")
+    ap.add_argument("--kary-mode", type=int, default=6, help="0 warp, 1 hybrid, 2-5 tiered, 6 thread-per-lookup, 7 + flat table")
     ap.add_argument("--no-naive", action="store_true", help="skip the naive comparison leg")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=1 << 22)
@@ -217,7 +217,7 @@ def main():
     dq = P.as_torch(q)
     out = torch.empty(m, dtype={4: torch.int32, 8: torch.int64}[ob], device="cuda")
 
-    K = args.k or 9
+    K = args.k or 5
     C = args.leaf_chunk or 16
     lay = bs.bs_layout_default(key_bytes=kb, out_bytes=ob, variant=VARIANTS[args.variant], k=K, leaf_chunk=C,
                                schedule=args.schedule, threads=args.threads, nreg=args.nreg,

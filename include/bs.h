@@ -93,7 +93,13 @@ typedef struct {
                                    shared-memory node, W*key/16 lanes per lookup with 16-B
                                    vector loads in L2/HBM (needs C/W in {1,2,4}, else mode 1);
                                3 = tiered with 8-B shared probes (u64: one slot plane instead
-                                   of hi/lo word planes; u32: same as 2)                     */
+                                   of hi/lo word planes; u32: same as 2);
+                               4/5 = 2/3 with a software pipeline across warp-tiles;
+                               6 = thread per lookup through the shared AND global separator
+                                   levels (node <= 64 B, 256-bit loads), C*key/32 lanes per
+                                   lookup for the leaf (needs C*key in 32..256 B, else 2);
+                               7 = 6 with the shared levels replaced by a binary search over
+                                   a pinned Eytzinger table of one level's node maxima     */
     uint32_t reserved[6];   /* must be 0                                                    */
 } bs_layout;
 
@@ -147,10 +153,10 @@ typedef struct {
 #define BS_EXPORT_PINNED 1   /* the level-major pinned table (pinned_entries keys)     */
 #define BS_EXPORT_KARY 2     /* K-ary separator slots, levels top-first (separator_slots) */
 
-/* Fills *l with defaults for u64 keys/outputs, K-ary K = 9 / C = 16 with the
- * tiered schedule (kary_mode 2; the fastest measured on B200 for 2^26 u64 keys,
- * the paper's A6000 optimum was K = 17), largest pin
- * budget, static schedule.  BS_ERR_INVALID if l is NULL. */
+/* Fills *l with defaults for u64 keys/outputs, K-ary K = 5 / C = 16 with the
+ * thread-per-lookup schedule (kary_mode 6; the fastest measured on B200 for
+ * 2^26 u64 keys, DESIGN.md §6.1 — the paper's A6000 optimum was K = 17,
+ * P:223), largest pin budget, static schedule.  BS_ERR_INVALID if l is NULL. */
 int bs_layout_default(bs_layout* l);
 
 /* Fills *l with the per-call defaults stored in idx. */

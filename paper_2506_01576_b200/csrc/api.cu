@@ -50,6 +50,8 @@ static void free_index(Index* ix) {
     if (ix->d_sep) cudaFree(ix->d_sep);
     if (ix->d_img) cudaFree(ix->d_img);
     if (ix->d_img64) cudaFree(ix->d_img64);
+    if (ix->d_flat) cudaFree(ix->d_flat);
+    if (ix->d_flat64) cudaFree(ix->d_flat64);
     destroy_host_ctx(ix);
     destroy_dist_state(ix);
     delete ix;
@@ -87,6 +89,8 @@ void table_prefix(const Index* ix, uint64_t entries, bool partial, uint32_t* D, 
     *D = d;
     *P = (uint32_t)p;
 }
+
+static uint64_t chunks_of(const Index* ix) { return (ix->n + ix->kC - 1) / ix->kC; }
 
 static int build_kary_layout(Index* ix, cudaStream_t st) {
     const uint64_t n = ix->n;
@@ -170,6 +174,34 @@ static int build_kary_layout(Index* ix, cudaStream_t st) {
             if (e != cudaSuccess) return fail_cuda(e, "build_kary_image(64)");
         }
     }
+    {   // flat pinned table: the deepest level (or the leaf chunks, level L) whose
+        // node maxima fit a complete Eytzinger tree of 2^D 4-B words in one CTA's
+        // shared memory
+        const uint64_t cap_words = ((uint64_t)ix->smem_optin - 1024 - 16) / 4;
+        uint32_t lt = 0;
+        for (uint32_t l = 0; l <= L; ++l) {
+            const uint64_t nl = (l < L) ? ix->k_nodes[l] : chunks_of(ix);
+            uint32_t D = 2;   // >= 4 slots: the TMA bulk copy moves multiples of 16 B
+            while ((1ull << D) - 1 < nl - 1) ++D;
+            if ((1ull << D) <= cap_words) lt = l;
+        }
+        const uint64_t nl = (lt < L) ? ix->k_nodes[lt] : chunks_of(ix);
+        uint32_t D = 2;
+        while ((1ull << D) - 1 < nl - 1) ++D;
+        uint64_t span = C;                                    // keys under one level-lt node
+        for (uint32_t l = lt; l < L; ++l) span *= K;
+        ix->flat_level = lt;
+        ix->flat_M = nl - 1;
+        ix->flat_D = D;
+        e = cudaMalloc(&ix->d_flat, 4ull << D);
+        if (e != cudaSuccess) return fail_cuda(e, "cudaMalloc(flat table)");
+        if (kb == 8) {
+            e = cudaMalloc(&ix->d_flat64, 8ull << D);
+            if (e != cudaSuccess) return fail_cuda(e, "cudaMalloc(flat table 64)");
+        }
+        e = build_flat_table(kb, ix->d_keys, n, span, ix->flat_M, D, ix->d_flat, ix->d_flat64, st);
+        if (e != cudaSuccess) return fail_cuda(e, "build_flat_table");
+    }
     return BS_OK;
 }
 
@@ -199,11 +231,11 @@ int bs_layout_default(bs_layout* l) {
     l->pin_bytes = 0xFFFFFFFFu;
     l->pin_partial = 1;
     l->reorder = BS_REORDER_NONE;
-    l->k = 9;
+    l->k = 5;
     l->leaf_chunk = 16;
     l->ctas_per_sm = 0;
     l->cache_hints = BS_HINT_STREAM_EVICT_FIRST | BS_HINT_LEAF_EVICT_FIRST;
-    l->kary_mode = 2;
+    l->kary_mode = 6;
     return BS_OK;
 }
 
@@ -226,7 +258,7 @@ int bs_build(const void* keys, uint64_t n, const bs_layout* layout_in, void** ou
     if (lay.variant > BS_VARIANT_KARY) return fail(BS_ERR_INVALID, "unknown variant %u", lay.variant);
     if (lay.schedule > BS_SCHED_STATIC) return fail(BS_ERR_INVALID, "unknown schedule %u", lay.schedule);
     if (lay.reorder > BS_REORDER_FULL) return fail(BS_ERR_INVALID, "unknown reorder %u", lay.reorder);
-    if (lay.kary_mode > 6) return fail(BS_ERR_INVALID, "unknown kary_mode %u", lay.kary_mode);
+    if (lay.kary_mode > 7) return fail(BS_ERR_INVALID, "unknown kary_mode %u", lay.kary_mode);
     if (lay.k < 2 || lay.k > 33) return fail(BS_ERR_INVALID, "K must be in [2, 33]");
     if (!is_pow2(lay.leaf_chunk) || lay.leaf_chunk > 256) return fail(BS_ERR_INVALID, "leaf_chunk must be a power of two <= 256");
     if (!reserved_zero(lay.reserved, 6)) return fail(BS_ERR_INVALID, "layout.reserved must be zero");
@@ -376,7 +408,7 @@ int bs_lookup_ex(const void* idx, const void* queries, uint64_t m, void* out, vo
     } else {
         bs_launch_default(idx, &L);
     }
-    if (L.kary_mode > 6) return fail(BS_ERR_INVALID, "bs_lookup: unknown kary_mode %u", L.kary_mode);
+    if (L.kary_mode > 7) return fail(BS_ERR_INVALID, "bs_lookup: unknown kary_mode %u", L.kary_mode);
     if (m == 0) return BS_OK;
     if (!queries || !out) return fail(BS_ERR_INVALID, "bs_lookup: NULL queries/out with m > 0");
     const uintptr_t q0 = (uintptr_t)queries, q1 = q0 + m * ix->kb;
@@ -416,6 +448,7 @@ int bs_index_info(const void* idx, bs_info* info) {
     info->footprint_bytes = info->array_bytes + ix->tab_entries * ix->kb + info->separator_bytes;
     if (ix->d_img) info->footprint_bytes += (uint64_t)ix->img_base[ix->img_L] * 4 * (ix->kb == 8 ? 2 : 1);
     if (ix->d_img64) info->footprint_bytes += (uint64_t)ix->img64_base[ix->img64_L] * 8;
+    if (ix->d_flat) info->footprint_bytes += (1ull << ix->flat_D) * (ix->d_flat64 ? 12 : 4);
     info->build_ms = ix->build_ms;
     info->sm_count = ix->sm_count;
     info->smem_per_cta_opt = (uint32_t)ix->last_opt_smem;

@@ -168,6 +168,49 @@ cudaError_t build_kary_image(int kb, const void* sep, uint32_t W, uint32_t L, co
     return cudaGetLastError();
 }
 
+// Flat pinned table in Eytzinger (BFS) order: slot k (1 <= k < 2^D) at depth
+// d = floor(log2 k) holds sorted entry i = (2(k - 2^d) + 1) 2^(D-1-d) - 1;
+// entry i < M = nodes - 1 is the max key of node i of the chosen K-ary level
+// (span keys per node), the rest are MAX.  Slot 0 is unused.  Probes at depth
+// d touch the contiguous slots [2^d, 2^(d+1)), so lanes spread over banks
+// (a plain sorted array makes every lane of a halving step hit one bank).
+template <class K>
+__global__ void k_build_flat(const K* __restrict__ a, uint64_t n, uint64_t span, uint64_t M, uint32_t D,
+                             uint32_t* __restrict__ f32, uint64_t* __restrict__ f64) {
+    const uint64_t slots = 1ull << D;
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < slots;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        K v = KeyMax<K>::v;
+        if (k > 0) {
+            const uint32_t d = 63 - __clzll((long long)k);
+            const uint64_t i = ((2 * (k - (1ull << d)) + 1) << (D - 1 - d)) - 1;
+            if (i < M) {
+                uint64_t end = (i + 1) * span;
+                if (end > n) end = n;
+                v = a[end - 1];
+            }
+        }
+        if constexpr (sizeof(K) == 8) {
+            f32[k] = (uint32_t)((uint64_t)v >> 32);
+            f64[k] = (uint64_t)v;
+        } else {
+            f32[k] = (uint32_t)v;
+        }
+    }
+}
+
+cudaError_t build_flat_table(int kb, const void* a, uint64_t n, uint64_t span, uint64_t M, uint32_t D,
+                             void* flat32, void* flat64, cudaStream_t s) {
+    const uint64_t slots = 1ull << D;
+    if (kb == 8)
+        k_build_flat<uint64_t><<<grid_for(slots, 256), 256, 0, s>>>((const uint64_t*)a, n, span, M, D,
+                                                                    (uint32_t*)flat32, (uint64_t*)flat64);
+    else
+        k_build_flat<uint32_t><<<grid_for(slots, 256), 256, 0, s>>>((const uint32_t*)a, n, span, M, D,
+                                                                    (uint32_t*)flat32, nullptr);
+    return cudaGetLastError();
+}
+
 cudaError_t build_sort_keys(int kb, const void* in, void* out, uint64_t n, cudaStream_t s) {
     size_t tmp_bytes = 0;
     cudaError_t e;

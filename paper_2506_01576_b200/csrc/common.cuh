@@ -158,6 +158,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 // shared memory with TMA bulk copies issued by one thread; every thread of the
 // CTA returns once the bytes have landed.  `bar` is a CTA-shared mbarrier.
 __device__ __forceinline__ void stage_to_smem(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    if (bytes % 16u != 0u) __trap();   // bulk copies move 16-B multiples; never wait forever
     if (threadIdx.x == 0) {
         mbar_init(bar, 1);
         fence_mbar_init();

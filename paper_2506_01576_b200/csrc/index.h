@@ -51,6 +51,16 @@ struct Index {
     void* d_img64 = nullptr;
     uint32_t img64_L = 0;
     uint32_t img64_base[kMaxKaryLevels + 1] = {};
+    // flat pinned table (kary_mode 7): the maxima of the nodes of K-ary level
+    // flat_level except the last node, in Eytzinger order — §4.2's pinned top of a binary
+    // search, placed over the K-ary levels.  A binary search over it yields the
+    // level-flat_level node directly (~log2 M probes instead of ~1.3x as many
+    // node by node).  d_flat: hi words (u64) or keys (u32), staged in shared
+    // memory; d_flat64: the exact u64 copy for the tie redo.
+    void* d_flat = nullptr;
+    void* d_flat64 = nullptr;
+    uint64_t flat_M = 0;             // node maxima stored (nodes - 1)
+    uint32_t flat_level = 0, flat_D = 0;   // Eytzinger slots 1..2^flat_D - 1
 
     // device
     int sm_count = 148, smem_optin = 232448, smem_per_sm = 233472, l2_bytes = 0;

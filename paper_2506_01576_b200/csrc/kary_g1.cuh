@@ -5,6 +5,10 @@
 // tiered schedule (kary_tiered.cuh) runs into on B200 — issue slots and L1
 // data-pipe wavefronts:
 //
+//  * FLAT (kary_mode 7): the shared-memory levels are replaced by ONE binary
+//    search over a pinned Eytzinger table of the maxima of the nodes of one
+//    K-ary level (Index::d_flat) — §4.2's pinned top levels of a binary search
+//    feeding §5's K-ary levels; D probes, no per-level bookkeeping.
 //  * shared-memory levels: ONE thread per lookup, binary search inside each
 //    node over the image's hi-word plane only (u64; u32 keys are exact).  A
 //    hi-word tie sets a flag and the warp redoes those levels exactly from
@@ -39,7 +43,7 @@ __device__ __forceinline__ void ld_node(const K* p, bool hint, uint64_t pol, K* 
     }
 }
 
-template <class K, int W, int GL, int IL, int T>
+template <class K, int W, int GL, int IL, int T, bool FLAT>
 __global__ void __launch_bounds__(1024, 1)
 k_kary_g1(const KaryParams<K> p, const K* __restrict__ q, uint64_t m, void* __restrict__ out, uint32_t ob) {
     constexpr int VL = 32 / (int)sizeof(K);     // leaf keys per lane (one 256-bit load)
@@ -56,7 +60,8 @@ k_kary_g1(const KaryParams<K> p, const K* __restrict__ q, uint64_t m, void* __re
     const uint32_t gl = lane / GL;               // leaf group within the warp
     const uint32_t gm = GMASK << (gl * GL);
 
-    if (p.img_words) stage_image<uint32_t, false>(S, p.img, p.img_plane_words, p.img_words, bar);
+    if (FLAT) stage_image<uint32_t, false>(S, p.flat, 0, 1u << p.flat_D, bar);
+    else if (p.img_words) stage_image<uint32_t, false>(S, p.img, p.img_plane_words, p.img_words, bar);
 
     const uint64_t pol_first = policy_evict_first();
     const uint64_t pol_last = policy_evict_last();
@@ -102,6 +107,42 @@ k_kary_g1(const KaryParams<K> p, const K* __restrict__ q, uint64_t m, void* __re
         bool tie = false;
 #pragma unroll
         for (int t = 0; t < T; ++t) node[t] = 0;
+        if constexpr (FLAT) {
+            // binary search over the pinned Eytzinger table of level-Ls node maxima:
+            // k <- 2k + [T[k] < q] for D levels; the rank k - 2^D is the node
+            const uint32_t D = p.flat_D;
+            uint32_t k[T];
+#pragma unroll
+            for (int t = 0; t < T; ++t) k[t] = 1;
+#pragma unroll 4
+            for (uint32_t d = 0; d < D; ++d) {
+#pragma unroll
+                for (int t = 0; t < T; ++t) {
+                    const uint32_t h = S[k[t]];
+                    bool less;
+                    if constexpr (sizeof(K) == 8) {
+                        const uint32_t qh = (uint32_t)((uint64_t)key[t] >> 32);
+                        less = h < qh;
+                        tie |= h == qh;
+                    } else {
+                        less = h < (uint32_t)key[t];
+                    }
+                    k[t] = 2 * k[t] + (less ? 1u : 0u);
+                }
+            }
+            if constexpr (sizeof(K) == 8) {
+                if (__any_sync(0xFFFFFFFFu, tie)) {
+#pragma unroll 1
+                    for (int t = 0; t < T; ++t) {
+                        k[t] = 1;
+                        for (uint32_t d = 0; d < D; ++d)
+                            k[t] = 2 * k[t] + ((ldg(p.flat64 + k[t]) < (uint64_t)key[t]) ? 1u : 0u);
+                    }
+                }
+            }
+#pragma unroll
+            for (int t = 0; t < T; ++t) node[t] = k[t] - (1u << D);
+        } else {
         for (uint32_t l = 0; l < Ls; ++l) {
             const uint32_t last = p.nodes_next[l] - 1;
             const uint32_t base = p.img_base[l];
@@ -122,6 +163,7 @@ k_kary_g1(const KaryParams<K> p, const K* __restrict__ q, uint64_t m, void* __re
                     node[t] = child < last ? child : last;
                 }
             }
+        }
         }
         // ---- global separator levels: thread per lookup, whole node in registers ----
         for (uint32_t l = Ls; l < L; ++l) {
@@ -187,8 +229,9 @@ k_kary_g1(const KaryParams<K> p, const K* __restrict__ q, uint64_t m, void* __re
 
 template <class K, int W, int GL, int IL>
 static cudaError_t go_g1(const void* params, const void* q, uint64_t m, void* out, uint32_t ob, uint32_t threads,
-                         uint32_t T, Grid grid, uint32_t smem, cudaStream_t s, bool* uns) {
-    auto kern = T >= 2 ? k_kary_g1<K, W, GL, IL, 2> : k_kary_g1<K, W, GL, IL, 1>;
+                         uint32_t T, bool flat, Grid grid, uint32_t smem, cudaStream_t s, bool* uns) {
+    auto kern = flat ? (T >= 2 ? k_kary_g1<K, W, GL, IL, 2, true> : k_kary_g1<K, W, GL, IL, 1, true>)
+                     : (T >= 2 ? k_kary_g1<K, W, GL, IL, 2, false> : k_kary_g1<K, W, GL, IL, 1, false>);
     cudaFuncAttributes fa;
     cudaError_t e = cudaFuncGetAttributes(&fa, kern);
     if (e != cudaSuccess) return e;
@@ -216,13 +259,13 @@ static cudaError_t go_g1(const void* params, const void* q, uint64_t m, void* ou
 // W = node slots (W*key <= 64 B), GL = leaf lanes (C*key = 32*GL), IL = leaf waves in flight
 template <class K>
 cudaError_t dispatch_g1(const void* params, const void* q, uint64_t m, void* out, uint32_t ob, uint32_t threads,
-                        uint32_t W, uint32_t GL, uint32_t IL, uint32_t T, Grid grid, uint32_t smem, cudaStream_t s,
-                        bool* uns) {
+                        uint32_t W, uint32_t GL, uint32_t IL, uint32_t T, bool flat, Grid grid, uint32_t smem,
+                        cudaStream_t s, bool* uns) {
 #define BS_G1_IL(WW, GG)                                                                                  \
     {                                                                                                     \
-        if (IL >= 4 && GG >= 4) return go_g1<K, WW, GG, (GG >= 4 ? 4 : 1)>(params, q, m, out, ob, threads, T, grid, smem, s, uns); \
-        if (IL >= 2 && GG >= 2) return go_g1<K, WW, GG, (GG >= 2 ? 2 : 1)>(params, q, m, out, ob, threads, T, grid, smem, s, uns); \
-        return go_g1<K, WW, GG, 1>(params, q, m, out, ob, threads, T, grid, smem, s, uns);                  \
+        if (IL >= 4 && GG >= 4) return go_g1<K, WW, GG, (GG >= 4 ? 4 : 1)>(params, q, m, out, ob, threads, T, flat, grid, smem, s, uns); \
+        if (IL >= 2 && GG >= 2) return go_g1<K, WW, GG, (GG >= 2 ? 2 : 1)>(params, q, m, out, ob, threads, T, flat, grid, smem, s, uns); \
+        return go_g1<K, WW, GG, 1>(params, q, m, out, ob, threads, T, flat, grid, smem, s, uns);                  \
     }
 #define BS_G1_G(WW)                             \
     case WW:                                    \

@@ -3,5 +3,5 @@
 
 namespace bs {
 template cudaError_t dispatch_g1<uint64_t>(const void*, const void*, uint64_t, void*, uint32_t, uint32_t, uint32_t,
-                                           uint32_t, uint32_t, uint32_t, Grid, uint32_t, cudaStream_t, bool*);
+                                           uint32_t, uint32_t, uint32_t, bool, Grid, uint32_t, cudaStream_t, bool*);
 }  // namespace bs

@@ -152,6 +152,7 @@ __device__ __forceinline__ void stage_image(uint32_t* S, const uint32_t* img, ui
         fence_mbar_init();
     }
     __syncthreads();
+    if ((words * unit) % 16u != 0u) __trap();   // bulk copies move 16-B multiples; never wait forever
     if (threadIdx.x == 0) {
         mbar_arrive_expect_tx(bar, words * unit * planes);
         constexpr uint32_t CH = 32768;

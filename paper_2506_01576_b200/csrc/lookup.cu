@@ -111,7 +111,7 @@ static int run_kary(const Index* ix, const void* q, uint64_t m, void* out, cudaS
     }
     const uint32_t W = ix->kW, C = ix->kC;
     const uint32_t GL = C * ix->kb / 32;
-    const bool g1 = L.kary_mode == 6 && W * ix->kb <= 64 && W * ix->kb >= 8 && C * ix->kb >= 32 &&
+    const bool g1 = (L.kary_mode == 6 || L.kary_mode == 7) && W * ix->kb <= 64 && W * ix->kb >= 8 && C * ix->kb >= 32 &&
                     C * ix->kb <= 256;
     const bool tiered = !g1 && L.kary_mode >= 2 && C >= W && (C / W == 1 || C / W == 2 || C / W == 4);
     const bool pair64 = (L.kary_mode == 3 || L.kary_mode == 5) && ix->kb == 8;
@@ -150,12 +150,21 @@ static int run_kary(const Index* ix, const void* q, uint64_t m, void* out, cudaS
         for (uint32_t l = 0; l < Li; ++l) p.img_base[l] = ix->img_base[l];
         p.img_words = ix->img_base[Li];
         p.smem_bytes = p.img_words * 4 + 16;
+        const bool flat = L.kary_mode == 7 && ix->d_flat && stat && L.use_pinned &&
+                          (4ull << ix->flat_D) + 16 <= smem_cap(ix, L.ctas_per_sm ? L.ctas_per_sm : 1);
+        if (flat) {
+            p.Ls = ix->flat_level;
+            p.flat = (const uint32_t*)ix->d_flat;
+            p.flat64 = (const uint64_t*)ix->d_flat64;
+            p.flat_D = ix->flat_D;
+            p.smem_bytes = (4u << ix->flat_D) + 16;
+        }
         ix->last_kary_smem = p.smem_bytes;
         // nreg: low 4 bits = leaf waves in flight IL (default 4), bits 4.. = lookups
         // per thread T (1 or 2, default 1)
         const uint32_t IL = (L.nreg & 15) ? (L.nreg & 15) : 4;
         const uint32_t T = (L.nreg >> 4) ? (L.nreg >> 4) : 1;
-        cudaError_t e = launch_kary_g1(ix->kb, ix->ob, &p, q, m, out, threads, W, GL, IL, T, g, p.smem_bytes, s, &uns);
+        cudaError_t e = launch_kary_g1(ix->kb, ix->ob, &p, q, m, out, threads, W, GL, IL, T, flat, g, p.smem_bytes, s, &uns);
         if (uns) return fail(BS_ERR_UNSUPPORTED, "KARY g1: threads=%u W=%u C=%u not supported", threads, W, C);
         if (e != cudaSuccess) return fail_cuda(e, "KARY g1 launch");
         return BS_OK;

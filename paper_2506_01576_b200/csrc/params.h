@@ -52,6 +52,10 @@ struct KaryParams {
     uint64_t img_plane_words;// words per plane in global memory
     uint32_t img_base[kMaxKaryLevels];
     uint32_t img_words;      // words of each plane staged (img_base[Ls], 4-word multiple)
+    // flat pinned table (kary_mode 7): Eytzinger slots 1..2^flat_D-1 (hi words for u64)
+    const uint32_t* flat;    // staged from here (2^flat_D words; slot 0 unused)
+    const uint64_t* flat64;  // exact u64 copy (tie redo), u64 keys only
+    uint32_t flat_D;
 };
 
 // ---- launchers (return cudaGetLastError() after the launch) ----
@@ -87,8 +91,8 @@ cudaError_t launch_kary_tiered(int kb, int ob, const void* params, const void* q
 // thread-per-lookup K-ary (kary_g1.cuh, kary_mode 6): W*key <= 64 B nodes,
 // GL = C*key/32 leaf lanes, IL leaf waves in flight, T lookups per thread in flight
 cudaError_t launch_kary_g1(int kb, int ob, const void* params, const void* q, uint64_t m, void* out,
-                           uint32_t threads, uint32_t W, uint32_t GL, uint32_t IL, uint32_t T, Grid grid,
-                           uint32_t smem, cudaStream_t s, bool* unsupported);
+                           uint32_t threads, uint32_t W, uint32_t GL, uint32_t IL, uint32_t T, bool flat,
+                           Grid grid, uint32_t smem, cudaStream_t s, bool* unsupported);
 
 // ---- build kernels ----
 cudaError_t build_check_sorted(int kb, const void* a, uint64_t n, int* d_flag, cudaStream_t s);
@@ -100,6 +104,8 @@ cudaError_t build_kary_levels(int kb, const void* a, uint64_t n, uint32_t K, uin
 cudaError_t build_kary_image(int kb, const void* sep, uint32_t W, uint32_t L, const uint64_t* lvl_base,
                               const uint64_t* lvl_nodes, const uint32_t* img_base, uint64_t plane_words,
                               void* img, bool pair64, cudaStream_t s);
+cudaError_t build_flat_table(int kb, const void* a, uint64_t n, uint64_t span, uint64_t M, uint32_t D,
+                             void* flat32, void* flat64, cudaStream_t s);
 cudaError_t build_sort_keys(int kb, const void* in, void* out, uint64_t n, cudaStream_t s);
 
 // ---- multi-GPU routing kernels (dist.cu) ----

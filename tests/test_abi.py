@@ -35,7 +35,7 @@ def test_layout_default_and_version():
     lay = bs.bs_layout_default()
     assert lay.struct_size == ctypes.sizeof(bs.bs_layout)
     assert lay.key_bytes == 8 and lay.out_bytes == 8
-    assert lay.variant == bs.KARY and lay.k == 9 and lay.leaf_chunk == 16 and lay.kary_mode == 2
+    assert lay.variant == bs.KARY and lay.k == 5 and lay.leaf_chunk == 16 and lay.kary_mode == 6
     assert "sm_100a" in bs.bs_version()
 
 

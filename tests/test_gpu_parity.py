@@ -146,7 +146,7 @@ def test_kary_k_c_waves(kb):
     for K in (2, 3, 4, 5, 8, 9, 16, 17, 32, 33):
         for C in (1, 2, 4, 8, 16, 32, 64):
             idx = build(keys, variant=bs.KARY, k=K, leaf_chunk=C)
-            for mode in (6, 5, 4, 3, 2, 1, 0):
+            for mode in (7, 6, 5, 4, 3, 2, 1, 0):
                 for R, sched, pin in ((1, bs.STATIC, 1), (2, bs.DYNAMIC, 0), (4, bs.STATIC, 0), (8, bs.STATIC, 1)):
                     got = run(idx, q, kb, variant=bs.KARY, nreg=R, schedule=sched, use_pinned=pin,
                               threads=256 if R < 8 else 128, kary_mode=mode)
@@ -162,7 +162,7 @@ def test_kary_tiered_out_widths(kb, ob):
     want = oracle.lookup(keys, q, out_bytes=ob)
     for K, C in ((17, 16), (16, 16), (9, 16), (5, 8), (33, 32), (3, 4), (9, 32), (5, 16), (4, 16), (3, 16), (8, 32)):
         idx = build(keys, variant=bs.KARY, k=K, leaf_chunk=C, out_bytes=ob)
-        for mode in (2, 3, 4, 5, 6):
+        for mode in (2, 3, 4, 5, 6, 7):
             for I in (1, 2, 4):
                 check(run(idx, q, ob, kary_mode=mode, nreg=I), want, q, f"tiered{mode} K={K} C={C} I={I} kb={kb} ob={ob}")
         idx.close()
@@ -175,7 +175,7 @@ def test_kary_small_n_all_shapes():
                 keys = edge_keys(n, 8, seed=n * 7 + K)
                 q = workload.adversarial_queries(keys, seed=K, extra=50)
                 idx = build(keys, variant=bs.KARY, k=K, leaf_chunk=C)
-                for mode in (6, 5, 4, 3, 2, 1, 0):
+                for mode in (7, 6, 5, 4, 3, 2, 1, 0):
                     check(run(idx, q, 8, kary_mode=mode), oracle.lookup(keys, q), q, f"n={n} K={K} C={C} mode={mode}")
 
 

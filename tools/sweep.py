@@ -107,6 +107,21 @@ def main():
                     measure(idx, rec, variant=bs.KARY, threads=t, nreg=R, schedule=sched, use_pinned=pin,
                             cache_hints=hints, kary_mode=mode)
             idx.close()
+    if "ladder" in what:
+        # the paper's §4 optimisation ladder (Figs. 4/6/8 analogues): scheduling,
+        # steps- vs full-pinning, lookup- vs full-reordering, on the OPT kernel
+        idx = bs.bs_build(dk, n, bs.bs_layout_default(key_bytes=kb, out_bytes=kb, variant=bs.OPT))
+        measure(idx, {"variant": "naive", "step": "naive dynamic 256"}, variant=bs.NAIVE, threads=256)
+        for t, nreg in ((256, 4), (256, 8), (512, 4), (1024, 2)):
+            steps = [("static", dict(use_pinned=0, reorder=0, pin_partial=0)),
+                     ("static+steps-pinning", dict(use_pinned=1, reorder=0, pin_partial=0)),
+                     ("static+full-pinning", dict(use_pinned=1, reorder=0, pin_partial=1)),
+                     ("+lookup-reordering", dict(use_pinned=1, reorder=1, pin_partial=1)),
+                     ("+full-reordering", dict(use_pinned=1, reorder=2, pin_partial=1))]
+            for name, kw in steps:
+                rec = {"variant": "opt", "step": name, "threads": t, "nreg": nreg}
+                measure(idx, rec, variant=bs.OPT, threads=t, nreg=nreg, schedule=bs.STATIC, **kw)
+        idx.close()
     if "opt" in what:
         idx = bs.bs_build(dk, n, bs.bs_layout_default(key_bytes=kb, out_bytes=kb, variant=bs.OPT))
         grid = itertools.product([128, 256, 512, 1024], [1, 2, 4, 8, 16], [0, 1, 2], [1, 0], [bs.STATIC])
