@@ -1,32 +1,34 @@
 // host.cu — bs_lookup_host: end-to-end lookups from host memory.
 //
-// Chunked 3-stream pipeline: for chunk c on stream c % 3:
+// Chunked S-stream pipeline (S = 4 by default): for chunk c on stream c % S:
 //   H2D(queries chunk) -> bs lookup kernel -> D2H(results chunk)
 // so the PCIe copy of chunk c+1 overlaps the kernel of chunk c and the
 // copy-back of chunk c-1 (H2D and D2H use separate copy engines).  Pageable
 // host buffers are staged through pinned buffers by the calling thread.
+#include <cstdlib>
 #include <cstring>
 
 #include "index.h"
 
 namespace bs {
 
-constexpr int kStages = 3;
+constexpr int kMaxStages = 8;
 
 struct HostCtx {
     uint64_t chunk = 0;                 // queries per chunk
-    cudaStream_t st[kStages] = {};
-    cudaEvent_t done[kStages] = {};
-    void* dq[kStages] = {};
-    void* dout[kStages] = {};
-    void* hq[kStages] = {};             // pinned staging (pageable callers only)
-    void* hout[kStages] = {};
+    int stages = 4;                     // buffers / streams in the ring
+    cudaStream_t st[kMaxStages] = {};
+    cudaEvent_t done[kMaxStages] = {};
+    void* dq[kMaxStages] = {};
+    void* dout[kMaxStages] = {};
+    void* hq[kMaxStages] = {};          // pinned staging (pageable callers only)
+    void* hout[kMaxStages] = {};
 };
 
 void destroy_host_ctx(Index* ix) {
     HostCtx* h = ix->host;
     if (!h) return;
-    for (int i = 0; i < kStages; ++i) {
+    for (int i = 0; i < kMaxStages; ++i) {
         if (h->st[i]) cudaStreamSynchronize(h->st[i]);
         if (h->dq[i]) cudaFree(h->dq[i]);
         if (h->dout[i]) cudaFree(h->dout[i]);
@@ -42,8 +44,17 @@ void destroy_host_ctx(Index* ix) {
 static int make_ctx(Index* ix) {
     HostCtx* h = new HostCtx();
     h->chunk = 1ull << 22;   // 4 Mi queries: 32 MB per buffer at u64
+    // tuning knobs for the copy pipeline (not part of the ABI)
+    if (const char* e = getenv("BS_HOST_CHUNK_LOG2")) {
+        const int v = atoi(e);
+        if (v >= 16 && v <= 26) h->chunk = 1ull << v;
+    }
+    if (const char* e = getenv("BS_HOST_STAGES")) {
+        const int v = atoi(e);
+        if (v >= 2 && v <= kMaxStages) h->stages = v;
+    }
     ix->host = h;
-    for (int i = 0; i < kStages; ++i) {
+    for (int i = 0; i < h->stages; ++i) {
         cudaError_t e = cudaStreamCreateWithFlags(&h->st[i], cudaStreamNonBlocking);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->done[i], cudaEventDisableTiming);
         if (e == cudaSuccess) e = cudaMalloc(&h->dq[i], h->chunk * ix->kb);
@@ -89,15 +100,15 @@ extern "C" int bs_lookup_host(const void* idx, const void* host_q, uint64_t m, v
     cudaEvent_t ev0;
     cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming);
     cudaEventRecord(ev0, (cudaStream_t)stream);
-    for (int i = 0; i < kStages; ++i) cudaStreamWaitEvent(h->st[i], ev0, 0);
+    for (int i = 0; i < h->stages; ++i) cudaStreamWaitEvent(h->st[i], ev0, 0);
     cudaEventDestroy(ev0);
 
     const uint64_t nch = (m + h->chunk - 1) / h->chunk;
-    uint64_t pend_off[kStages] = {}, pend_cnt[kStages] = {};
-    bool pend[kStages] = {};
+    uint64_t pend_off[kMaxStages] = {}, pend_cnt[kMaxStages] = {};
+    bool pend[kMaxStages] = {};
     int rc = BS_OK;
     for (uint64_t c = 0; c < nch && rc == BS_OK; ++c) {
-        const int b = (int)(c % kStages);
+        const int b = (int)(c % (uint64_t)h->stages);
         const uint64_t off = c * h->chunk;
         const uint64_t cnt = (m - off < h->chunk) ? (m - off) : h->chunk;
         cudaStream_t s = h->st[b];
@@ -123,7 +134,7 @@ extern "C" int bs_lookup_host(const void* idx, const void* host_q, uint64_t m, v
         pend_off[b] = off;
         pend_cnt[b] = cnt;
     }
-    for (int b = 0; b < kStages; ++b) {
+    for (int b = 0; b < h->stages; ++b) {
         cudaError_t e = cudaStreamSynchronize(h->st[b]);
         if (e != cudaSuccess && rc == BS_OK) rc = fail_cuda(e, "bs_lookup_host sync");
         if (pend[b] && rc == BS_OK && !pin_o)

@@ -227,11 +227,146 @@ k_kary_g1(const KaryParams<K> p, const K* __restrict__ q, uint64_t m, void* __re
     }
 }
 
+// PIPE variant of the FLAT schedule (T = 1): the D probes of the NEXT
+// warp-tile's pinned-table search are spread over this tile's load stages
+// (global levels + leaf), so the shared-memory search costs issue slots but
+// never exposes its latency; the warp always has global loads in flight.
+template <class K, int W, int GL, int IL>
+__global__ void __launch_bounds__(1024, 1)
+k_kary_g1p(const KaryParams<K> p, const K* __restrict__ q, uint64_t m, void* __restrict__ out, uint32_t ob) {
+    constexpr int VL = 32 / (int)sizeof(K);
+    constexpr int GPWL = 32 / GL;
+    constexpr uint32_t GMASK = (GL == 32) ? 0xFFFFFFFFu : ((1u << GL) - 1u);
+    static_assert(GL >= 1 && 32 % GL == 0 && GL % IL == 0, "bad leaf shape");
+
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint32_t* S = reinterpret_cast<uint32_t*>(smem);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + p.smem_bytes - 16);
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t jl = lane % GL;
+    const uint32_t gl = lane / GL;
+    const uint32_t gm = GMASK << (gl * GL);
+
+    stage_image<uint32_t, false>(S, p.flat, 0, 1u << p.flat_D, bar);
+
+    const uint64_t pol_first = policy_evict_first();
+    const uint64_t pol_last = policy_evict_last();
+    const bool sh = p.stream_hint != 0, lh = p.leaf_hint != 0, sep_last = p.sep_hint != 0;
+    const uint64_t n = p.n;
+    const uint32_t K_ = p.K, C = p.C, L = p.L, Ls = p.Ls, D = p.flat_D;
+    const uint32_t fb_leaf = bitlen_c(C - 1);
+    const uint32_t stages = (L - Ls) + 1;
+    const uint32_t per = (D + stages - 1) / stages;   // probes of the next tile per load stage
+    const uint64_t warps_total = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint64_t nwt = (m + 31) / 32;
+    uint64_t wt = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+
+    auto load_tile = [&](uint64_t t) -> K {
+        const uint64_t i = t * 32 + lane;
+        return (t < nwt && i < m) ? load_stream(q + i, sh, pol_first) : KeyMax<K>::v;
+    };
+    auto probe = [&](uint32_t& k, K kq, bool& tie) {
+        const uint32_t h = S[k];
+        bool less;
+        if constexpr (sizeof(K) == 8) {
+            const uint32_t qh = (uint32_t)((uint64_t)kq >> 32);
+            less = h < qh;
+            tie |= h == qh;
+        } else {
+            less = h < (uint32_t)kq;
+        }
+        k = 2 * k + (less ? 1u : 0u);
+    };
+    auto exact = [&](K kq) -> uint32_t {
+        uint32_t k = 1;
+        for (uint32_t d = 0; d < D; ++d) k = 2 * k + ((ldg(p.flat64 + k) < (uint64_t)kq) ? 1u : 0u);
+        return k;
+    };
+
+    K key = load_tile(wt);
+    uint32_t node;
+    {
+        uint32_t k = 1;
+        bool tie = false;
+        for (uint32_t d = 0; d < D; ++d) probe(k, key, tie);
+        if constexpr (sizeof(K) == 8) {
+            if (__any_sync(0xFFFFFFFFu, tie)) k = exact(key);
+        }
+        node = k - (1u << D);
+    }
+    K key_n = load_tile(wt + warps_total);
+    K knext = load_tile(wt + 2 * warps_total);
+
+    for (; wt < nwt; wt += warps_total) {
+        uint32_t kn = 1, dn = 0;
+        bool tie_n = false;
+        // ---- global separator levels of tile t, next tile's probes in between ----
+        for (uint32_t l = Ls; l < L; ++l) {
+            K s[W];
+            ld_node<K, W>(p.sep + p.lvl_base[l] + (uint64_t)node * W, sep_last, pol_last, s);
+            for (uint32_t r = 0; r < per && dn < D; ++r, ++dn) probe(kn, key_n, tie_n);
+            uint32_t c = 0;
+#pragma unroll
+            for (int v = 0; v < W; ++v) c += (s[v] < key) ? 1u : 0u;
+            const uint32_t child = node * K_ + c;
+            const uint32_t last = p.nodes_next[l] - 1;
+            node = child < last ? child : last;
+        }
+        // ---- leaf of tile t ----
+#pragma unroll 1
+        for (int b = 0; b < GL / IL; ++b) {
+            K kk[IL];
+            uint32_t cc[IL];
+            K x[IL][VL];
+#pragma unroll
+            for (int i = 0; i < IL; ++i) {
+                const int src = (b * IL + i) * GPWL + (int)gl;
+                kk[i] = __shfl_sync(0xFFFFFFFFu, key, src);
+                cc[i] = __shfl_sync(0xFFFFFFFFu, node, src);
+                ldv<K, VL>(p.a + (uint64_t)cc[i] * C + jl * VL, lh, pol_first, x[i]);
+            }
+            for (; dn < D; ++dn) probe(kn, key_n, tie_n);
+#pragma unroll
+            for (int i = 0; i < IL; ++i) {
+                uint32_t lt = 0;
+                bool eq = false;
+#pragma unroll
+                for (int u = 0; u < VL; ++u) {
+                    if (u < VL - 1 || jl != GL - 1) lt += (x[i][u] < kk[i]) ? 1u : 0u;
+                    eq |= x[i][u] == kk[i];
+                }
+                const bool last_lt = x[i][VL - 1] < kk[i];
+                lt = group_sum<GL>(lt, gl, fb_leaf);
+                const bool any_eq = (__ballot_sync(0xFFFFFFFFu, eq) & gm) != 0;
+                if (jl == GL - 1) {
+                    const uint64_t lbv = (uint64_t)cc[i] * C + lt + (last_lt ? 1u : 0u);
+                    const bool hit = any_eq && lbv < n;
+                    const uint64_t miss = ob == 8 ? (1ull << 63) : (1ull << 31);
+                    const uint64_t res = hit ? lbv : (lbv | miss);
+                    const uint64_t o = wt * 32 + (uint64_t)((b * IL + i) * GPWL) + gl;
+                    if (o < m) {
+                        if (ob == 8) store_stream((uint64_t*)out + o, res, sh, pol_first);
+                        else store_stream((uint32_t*)out + o, (uint32_t)res, sh, pol_first);
+                    }
+                }
+            }
+        }
+        if constexpr (sizeof(K) == 8) {
+            if (__any_sync(0xFFFFFFFFu, tie_n)) kn = exact(key_n);
+        }
+        node = kn - (1u << D);
+        key = key_n;
+        key_n = knext;
+        knext = load_tile(wt + 3 * warps_total);
+    }
+}
+
 template <class K, int W, int GL, int IL>
 static cudaError_t go_g1(const void* params, const void* q, uint64_t m, void* out, uint32_t ob, uint32_t threads,
                          uint32_t T, bool flat, Grid grid, uint32_t smem, cudaStream_t s, bool* uns) {
     auto kern = flat ? (T >= 2 ? k_kary_g1<K, W, GL, IL, 2, true> : k_kary_g1<K, W, GL, IL, 1, true>)
                      : (T >= 2 ? k_kary_g1<K, W, GL, IL, 2, false> : k_kary_g1<K, W, GL, IL, 1, false>);
+    if (flat && T == 3) kern = k_kary_g1p<K, W, GL, IL>;   // T = 3 encodes "pipelined, one lookup per thread"
     cudaFuncAttributes fa;
     cudaError_t e = cudaFuncGetAttributes(&fa, kern);
     if (e != cudaSuccess) return e;

@@ -77,6 +77,20 @@ static int run_opt(const Index* ix, const void* q, uint64_t m, void* out, cudaSt
     uint64_t es = 1;
     while (es < (32ull * ix->n) / (l2 / 2)) es <<= 1;
     p.evict_step = es;
+    // L1-allocating loads for the first global levels whose probe lines fit
+    // ~96 KB of L1 (2^d positions per level, one 128-B line each at most)
+    {
+        const uint64_t lines_total = (ix->n * ix->kb + 127) / 128;
+        uint64_t cum = 0, l1s = ~0ull;
+        const uint32_t d0 = P ? D + 1 : D;   // first level of the global phase
+        for (uint32_t d = d0; d < ix->levels; ++d) {
+            const uint64_t lines = d < 63 ? ((1ull << d) < lines_total ? (1ull << d) : lines_total) : lines_total;
+            if (cum + lines > 768) break;
+            cum += lines;
+            l1s = ix->s0 >> d;
+        }
+        p.l1_step = l1s;
+    }
     p.stream_hint = (L.cache_hints & BS_HINT_STREAM_EVICT_FIRST) ? 1 : 0;
     p.leaf_hint = (L.cache_hints & BS_HINT_LEAF_EVICT_FIRST) ? 1 : 0;
     p.kmin = (K)ix->a_first;

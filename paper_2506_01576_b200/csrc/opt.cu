@@ -166,7 +166,9 @@ __global__ void k_bs_opt(const OptParams<K> p, const K* __restrict__ q, uint64_t
             }
         }
         // ---- global phase (l.33, reading R11): Listing 1 loop, NREG loads in flight ----
-        for (uint64_t step = sD; step > 0; step >>= 1) {
+        // upper global levels (step >= l1_step) with L1-allocating loads, as the
+        // naive kernel gets them; the deep levels with L1::no_allocate (+ hints)
+        auto global_step = [&](uint64_t step, bool l1) {
             const bool hint = p.leaf_hint && step < p.evict_step;
             const bool first = (step == sD);
             K x[NREG];
@@ -174,13 +176,17 @@ __global__ void k_bs_opt(const OptParams<K> p, const K* __restrict__ q, uint64_t
 #pragma unroll
             for (int r = 0; r < NREG; ++r) {
                 go[r] = (step <= off[r]) && !(first && ((skip >> r) & 1u));
-                x[r] = go[r] ? load_key(p.a + (off[r] - step), hint, pol) : (K)0;
+                if (l1) x[r] = go[r] ? ldg(p.a + (off[r] - step)) : (K)0;
+                else x[r] = go[r] ? load_key(p.a + (off[r] - step), hint, pol) : (K)0;
             }
 #pragma unroll
             for (int r = 0; r < NREG; ++r) {
                 if (go[r] && x[r] >= key[r]) { off[r] -= step; v[r] = x[r]; }
             }
-        }
+        };
+        uint64_t step = sD;
+        for (; step > 0 && step >= p.l1_step; step >>= 1) global_step(step, true);
+        for (; step > 0; step >>= 1) global_step(step, false);
 
         // ---- results (l.35-39) ----
         if (REORDER == 2) {

@@ -25,6 +25,7 @@ struct OptParams {
     uint32_t valid[kMaxLevels];
     uint32_t base[kMaxLevels];
     uint64_t evict_step;  // global-phase steps < evict_step use the evict_first hint
+    uint64_t l1_step;     // global-phase steps >= l1_step use L1-allocating loads (upper levels that fit L1)
     uint32_t stream_hint; // 1: queries/results with L2 evict_first
     uint32_t leaf_hint;   // 1: deep probes with L2 evict_first
     // block-local reordering (§4.3): bucket = min((q - kmin) >> shift, nbuckets-1)

@@ -1,0 +1,66 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py
+times (configs[1] and configs[2]: 2^20 u32 / 2^26 u64 keys, 2^27 queries).
+
+The oracle cannot run 2^27 bisections in a test's time budget, so (③):
+  * a deterministic sample of 2^16 outputs is compared with oracle.lookup
+    element by element;
+  * EVERY output is checked against the property that fixes lb uniquely —
+    a[lb-1] < q <= a[lb] (a[-1] = -inf, a[n] = +inf) — plus the hit bit
+    (hit <=> lb < n and a[lb] == q).  The check runs with torch gathers on the
+    GPU (test plumbing, not the product path); unsigned order is mapped to
+    signed order by flipping bit 63.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import workload
+
+torch = pytest.importorskip("torch")
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+import bench  # noqa: E402
+import paper_2506_01576_b200 as P  # noqa: E402
+from paper_2506_01576_b200 import bs  # noqa: E402
+
+
+def _ordered(t: torch.Tensor, kb: int) -> torch.Tensor:
+    """int64 view whose signed order is the unsigned order of the keys."""
+    if kb == 8:
+        return t ^ torch.tensor(-(1 << 63), dtype=torch.int64, device=t.device)
+    return t.to(torch.int64) & 0xFFFFFFFF
+
+
+def _check_invariant(dk, dq, out, n, kb):
+    miss_bit = 63 if kb == 8 else 31
+    o = out.to(torch.int64) & ((1 << 32) - 1) if kb == 4 else out
+    miss = ((o >> miss_bit) & 1).bool()
+    lb = o & ((1 << miss_bit) - 1)
+    assert int(lb.max()) <= n and int(lb.min()) >= 0
+    a = _ordered(dk, kb)
+    q = _ordered(dq, kb)
+    lo_ok = (lb == 0) | (a[(lb - 1).clamp(min=0)] < q)
+    hi_ok = (lb == n) | (q <= a[lb.clamp(max=n - 1)])
+    assert bool(lo_ok.all()), "a[lb-1] < q violated"
+    assert bool(hi_ok.all()), "q <= a[lb] violated"
+    hit = (lb < n) & (a[lb.clamp(max=n - 1)] == q)
+    assert bool((hit == ~miss).all()), "hit bit wrong"
+
+
+@pytest.mark.parametrize("cfg", ["config2", "config3"])
+def test_fullsize_bench_launch(cfg):
+    n, kb, m, hr, _ = bench.CONFIGS[cfg]
+    keys, q, _ = bench.make_inputs(cfg, "random", 0)
+    dk, dq = P.as_torch(keys), P.as_torch(q)
+    out = torch.empty(m, dtype={4: torch.int32, 8: torch.int64}[kb], device="cuda")
+    # bench.py's launch configuration: the layout defaults (K, C, kary_mode, threads, nreg)
+    lay = bs.bs_layout_default(key_bytes=kb, out_bytes=kb)
+    idx = bs.bs_build(dk, n, lay)
+    bs.bs_lookup(idx, dq, m, out)
+    torch.cuda.synchronize()
+    samp = np.random.default_rng(11).integers(0, m, size=1 << 16)
+    got = P.to_numpy_unsigned(out, kb)[samp]
+    want = oracle.lookup(keys, q[samp], out_bytes=kb)
+    assert np.array_equal(got, want)
+    _check_invariant(dk, dq, out, n, kb)
+    idx.close()

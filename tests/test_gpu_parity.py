@@ -163,7 +163,7 @@ def test_kary_tiered_out_widths(kb, ob):
     for K, C in ((17, 16), (16, 16), (9, 16), (5, 8), (33, 32), (3, 4), (9, 32), (5, 16), (4, 16), (3, 16), (8, 32)):
         idx = build(keys, variant=bs.KARY, k=K, leaf_chunk=C, out_bytes=ob)
         for mode in (2, 3, 4, 5, 6, 7):
-            for I in (1, 2, 4):
+            for I in (1, 2, 4) if mode < 6 else (1, 2, 4, 0x24, 0x34):   # g1: T=2 / pipelined (T=3)
                 check(run(idx, q, ob, kary_mode=mode, nreg=I), want, q, f"tiered{mode} K={K} C={C} I={I} kb={kb} ob={ob}")
         idx.close()
 
