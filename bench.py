@@ -86,7 +86,12 @@ class ClockSampler:
                                        stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self._t = threading.Thread(target=self._read, daemon=True)
             self._t.start()
-            time.sleep(0.05)
+            # nvidia-smi can take ~1 s to emit its first line: wait for it so the
+            # samples cover the timed region, then drop the pre-region ones
+            t_end = time.time() + 5.0
+            while not self.samples and time.time() < t_end and self._p.poll() is None:
+                time.sleep(0.01)
+            self.samples.clear()
         except Exception:
             self._p = None
         return self
