@@ -280,6 +280,67 @@ int bs_lookup_dist(const void* idx, const void* local_queries, uint64_t m_local,
 /* Destroys the communicator (after all dist indexes using it). NULL-safe. */
 void bs_dist_destroy(void* comm);
 
+/* ------------------------------------------------------------------------
+ * Fused peer-memory routing (PARTITIONED mode without NCCL; SURVEY §8f f1,
+ * BASELINE.json config 5; not in the paper).  Same result contract as
+ * bs_lookup_dist in PARTITIONED mode: out_local[i] = base_s + lb_s(q_i)
+ * (| bit 63 on a miss), s = first shard whose maximum is >= q_i (else the
+ * last).  The exchange runs inside the kernels over CUDA-IPC-mapped peer
+ * memory (NVLink / NVSwitch P2P): the route kernel stores each query into
+ * its owner's receive window, the K-ary lookup kernel (kary_mode 6/7) stores
+ * each result into its source rank's return window, and monotonic device
+ * counters replace the host sync and the NCCL all-to-alls.
+ *
+ * Setup, per rank (one process per GPU; also valid for several processes
+ * sharing one GPU, which is how it is tested on a 1-GPU box):
+ *   bs_build_peer -> bs_peer_export -> (caller all-gathers the blobs, e.g.
+ *   torch.distributed.all_gather_object) -> bs_peer_connect.
+ * ---------------------------------------------------------------------- */
+
+/* Bytes of one rank's connection blob (host memory). */
+#define BS_PEER_BLOB_BYTES 256
+
+/* Builds this rank's index over its local ascending keys (device pointer,
+ * n_local >= 1; layout must give variant KARY and out_bytes 8) and allocates
+ * its IPC-exportable window: receive slots (recv_capacity keys + 8-B tags;
+ * 0 = world * max_m_local, which can never overflow) and a return window of
+ * max_m_local results.  max_m_local < 2^32 bounds m_local of later lookups.
+ * Not collective.  Errors: BS_ERR_INVALID (bad rank/world/sizes/layout),
+ * BS_ERR_UNSUPPORTED (variant is not KARY), BS_ERR_OOM, plus bs_build's. */
+int bs_build_peer(const void* local_keys, uint64_t n_local, const bs_layout* layout, int rank, int world,
+                  uint64_t max_m_local, uint64_t recv_capacity, void** out_idx);
+
+/* Writes this rank's connection blob (BS_PEER_BLOB_BYTES host bytes: the
+ * window's cudaIpcMemHandle_t, shard size and min/max key). */
+int bs_peer_export(const void* idx, void* blob);
+
+/* blobs = world consecutive blobs in rank order (host memory).  Checks that
+ * the shards are globally ordered (BS_ERR_NOT_SORTED otherwise), derives each
+ * shard's global base rank, maps every peer's window (cudaIpcOpenMemHandle,
+ * lazy peer access).  Once per index; not collective, but every rank must
+ * connect before any rank calls bs_lookup_peer. */
+int bs_peer_connect(void* idx, const void* blobs);
+
+/* Collective (every rank calls it, in the same order, m_local may be 0):
+ * route -> lookup -> return, three kernels on `stream`, stream-ordered and
+ * asynchronous, no host sync, no allocation.  local_queries: m_local keys;
+ * out_local: m_local u64 global results (device pointers, must not overlap
+ * the index's windows), or NULL to leave the results in the return window
+ * (bs_peer_results; saves one copy, valid until the next call).  A peer that never joins makes the waits time out
+ * after 20 s (error bit 2 in bs_peer_status, results undefined) instead of
+ * hanging the GPU.  Not thread-safe per index. */
+int bs_lookup_peer(const void* idx, const void* local_queries, uint64_t m_local, void* out_local, void* stream);
+
+/* *results = device pointer of this rank's return window: after a
+ * bs_lookup_peer with out_local == NULL, results[i] is query i's global
+ * result once the call's stream work has completed. */
+int bs_peer_results(const void* idx, const void** results);
+
+/* Synchronous diagnostic: *err_bits = OR of 1 (a receive window overflowed:
+ * recv_capacity too small, queries dropped) and 2 (a wait timed out) since
+ * build; *calls (may be NULL) = bs_lookup_peer calls issued. */
+int bs_peer_status(const void* idx, uint32_t* err_bits, uint64_t* calls);
+
 #ifdef __cplusplus
 }
 #endif

@@ -96,9 +96,16 @@ def lib():
         L.bs_lookup_dist.argtypes = [vp, vp, _u64, vp, vp]
         L.bs_dist_destroy.argtypes = [vp]
         L.bs_dist_destroy.restype = None
+        L.bs_build_peer.argtypes = [vp, _u64, ctypes.POINTER(bs_layout), i, i, _u64, _u64, ctypes.POINTER(vp)]
+        L.bs_peer_export.argtypes = [vp, vp]
+        L.bs_peer_connect.argtypes = [vp, vp]
+        L.bs_lookup_peer.argtypes = [vp, vp, _u64, vp, vp]
+        L.bs_peer_status.argtypes = [vp, ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(_u64)]
+        L.bs_peer_results.argtypes = [vp, ctypes.POINTER(vp)]
         for f in ("bs_layout_default", "bs_launch_default", "bs_build", "bs_lookup", "bs_lookup_ex",
                   "bs_lookup_host", "bs_index_info", "bs_export", "bs_dist_get_uid", "bs_dist_init",
-                  "bs_build_dist", "bs_lookup_dist"):
+                  "bs_build_dist", "bs_lookup_dist", "bs_build_peer", "bs_peer_export", "bs_peer_connect",
+                  "bs_lookup_peer", "bs_peer_status", "bs_peer_results"):
             getattr(L, f).restype = i
         _lib = L
     return _lib
@@ -259,3 +266,58 @@ def bs_lookup_dist(index: Index, local_queries, m_local: int, out_local, stream=
 
 def bs_dist_destroy(comm: int):
     lib().bs_dist_destroy(comm)
+
+
+# ---- fused peer-memory routing (include/bs.h "Fused peer-memory routing") ----
+PEER_BLOB_BYTES = 256
+
+
+def bs_build_peer(local_keys, n_local: int, layout: bs_layout | None, rank: int, world: int, max_m_local: int,
+                  recv_capacity: int = 0) -> Index:
+    if layout is None:
+        layout = bs_layout_default(variant=2, out_bytes=8)
+    h = ctypes.c_void_p()
+    _check(lib().bs_build_peer(_ptr(local_keys), n_local, ctypes.byref(layout), rank, world, max_m_local,
+                               recv_capacity, ctypes.byref(h)))
+    return Index(h.value, layout)
+
+
+def bs_peer_export(index: Index) -> bytes:
+    buf = ctypes.create_string_buffer(PEER_BLOB_BYTES)
+    _check(lib().bs_peer_export(index.handle, buf))
+    return buf.raw
+
+
+def bs_peer_connect(index: Index, blobs: list[bytes]):
+    raw = b"".join(blobs)
+    buf = ctypes.create_string_buffer(raw, len(raw))
+    return _check(lib().bs_peer_connect(index.handle, buf))
+
+
+def bs_peer_connect_group(index: Index, group=None):
+    """Argument marshalling only: all-gather the blobs over torch.distributed
+    (any backend) and connect."""
+    import torch.distributed as dist
+    blobs = [None] * dist.get_world_size(group)
+    dist.all_gather_object(blobs, bs_peer_export(index), group=group)
+    return bs_peer_connect(index, blobs)
+
+
+def bs_lookup_peer(index: Index, local_queries, m_local: int, out_local, stream=None):
+    return _check(lib().bs_lookup_peer(index.handle, _ptr(local_queries), m_local, _ptr(out_local),
+                                       _stream_ptr(stream)))
+
+
+def bs_peer_status(index: Index) -> tuple[int, int]:
+    err = ctypes.c_uint32()
+    calls = _u64()
+    _check(lib().bs_peer_status(index.handle, ctypes.byref(err), ctypes.byref(calls)))
+    return err.value, calls.value
+
+
+def bs_peer_results(index: Index) -> int:
+    """Device address of this rank's return window (results of the last
+    bs_lookup_peer called with out_local=None)."""
+    p = ctypes.c_void_p()
+    _check(lib().bs_peer_results(index.handle, ctypes.byref(p)))
+    return p.value

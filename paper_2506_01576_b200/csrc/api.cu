@@ -54,6 +54,7 @@ static void free_index(Index* ix) {
     if (ix->d_flat64) cudaFree(ix->d_flat64);
     destroy_host_ctx(ix);
     destroy_dist_state(ix);
+    destroy_peer_state(ix);
     delete ix;
 }
 

@@ -13,6 +13,21 @@ namespace bs {
 
 struct HostCtx;    // bs_lookup_host staging (host.cu)
 struct DistState;  // multi-GPU exchange state (dist.cu)
+struct PeerState;  // fused peer-memory routing state (peer.cu)
+
+// per-call arguments of the g1 kernel's peer prologue / epilogue (params.h)
+struct PeerLaunch {
+    unsigned long long* cursor;
+    const unsigned long long* wait;
+    unsigned long long target;
+    const uint64_t* tag;
+    uint64_t* const* ret;
+    unsigned long long* const* sig;
+    unsigned* done;
+    unsigned* err;
+    uint64_t base;
+    uint32_t P;
+};
 
 struct Index {
     bs_layout layout{};
@@ -73,6 +88,7 @@ struct Index {
 
     // multi-GPU
     DistState* dist = nullptr;
+    PeerState* peer = nullptr;
 };
 
 int fail(int code, const char* fmt, ...);
@@ -81,10 +97,13 @@ void table_prefix(const Index* ix, uint64_t entries, bool partial, uint32_t* D, 
 
 // lookup.cu
 int dispatch_lookup(const Index* ix, const void* q, uint64_t m, void* out, cudaStream_t s, const bs_launch& L);
+int dispatch_kary_peer(const Index* ix, const void* q, uint64_t cap, cudaStream_t s, const bs_launch& L,
+                       const PeerLaunch& pl);
 uint32_t kary_smem_levels(const Index* ix, uint32_t* bytes_out, uint64_t cap_bytes = 0);
 
 // host.cu / dist.cu
 void destroy_host_ctx(Index* ix);
 void destroy_dist_state(Index* ix);
+void destroy_peer_state(Index* ix);
 
 }  // namespace bs

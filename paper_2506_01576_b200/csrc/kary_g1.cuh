@@ -28,6 +28,7 @@
 #include "common.cuh"
 #include "kary_tiered.cuh"
 #include "params.h"
+#include "peer_sync.cuh"
 
 namespace bs {
 
@@ -45,7 +46,7 @@ __device__ __forceinline__ void ld_node(const K* p, bool hint, uint64_t pol, K* 
 
 template <class K, int W, int GL, int IL, int T, bool FLAT>
 __global__ void __launch_bounds__(1024, 1)
-k_kary_g1(const KaryParams<K> p, const K* __restrict__ q, uint64_t m, void* __restrict__ out, uint32_t ob) {
+k_kary_g1(const KaryParams<K> p, const K* __restrict__ q, uint64_t m_arg, void* __restrict__ out, uint32_t ob) {
     constexpr int VL = 32 / (int)sizeof(K);     // leaf keys per lane (one 256-bit load)
     constexpr int GPWL = 32 / GL;               // leaf lookups per wave
     constexpr uint32_t GMASK = (GL == 32) ? 0xFFFFFFFFu : ((1u << GL) - 1u);
@@ -62,6 +63,17 @@ k_kary_g1(const KaryParams<K> p, const K* __restrict__ q, uint64_t m, void* __re
 
     if (FLAT) stage_image<uint32_t, false>(S, p.flat, 0, 1u << p.flat_D, bar);
     else if (p.img_words) stage_image<uint32_t, false>(S, p.img, p.img_plane_words, p.img_words, bar);
+
+    // fused peer routing (bs_lookup_peer): wait until every rank has routed
+    // its queries into this rank's window; the slot count is on the device
+    const bool peer = p.peer_cursor != nullptr;
+    uint64_t m = m_arg;
+    if (peer) {
+        if (threadIdx.x == 0) peer_wait_ge(p.peer_wait, p.peer_wait_target, p.peer_err);
+        __syncthreads();
+        const uint64_t got = *(volatile const unsigned long long*)p.peer_cursor;
+        m = got < m_arg ? got : m_arg;
+    }
 
     const uint64_t pol_first = policy_evict_first();
     const uint64_t pol_last = policy_evict_last();
@@ -217,13 +229,28 @@ k_kary_g1(const KaryParams<K> p, const K* __restrict__ q, uint64_t m, void* __re
                     const uint64_t res = hit ? lbv : (lbv | miss);
                     const uint64_t o = (wt + t) * 32 + (uint64_t)((b * IL + i) * GPWL) + gl;
                     if (o < m) {
-                        if (ob == 8) store_stream((uint64_t*)out + o, res, sh, pol_first);
-                        else store_stream((uint32_t*)out + o, (uint32_t)res, sh, pol_first);
+                        if (peer) {
+                            // result straight into the source rank's return window (P2P store)
+                            const uint64_t tg = __ldcg(p.peer_tag + o);
+                            const uint64_t g = lbv + p.peer_base;
+                            p.peer_ret[tg >> 32][tg & 0xFFFFFFFFull] = hit ? g : (g | miss);
+                        } else if (ob == 8) {
+                            store_stream((uint64_t*)out + o, res, sh, pol_first);
+                        } else {
+                            store_stream((uint32_t*)out + o, (uint32_t)res, sh, pol_first);
+                        }
                     }
                 }
             }
         }
         }
+    }
+    if (peer && peer_last_cta(p.peer_done)) {
+        // every CTA has read the cursor (at its start) and stored its results:
+        // re-arm the window, then tell every rank its results have landed
+        *p.peer_cursor = 0;
+        __threadfence_system();
+        for (uint32_t r = 0; r < p.peer_P; ++r) red_release_sys_add_u64(p.peer_sig[r], 1ull);
     }
 }
 

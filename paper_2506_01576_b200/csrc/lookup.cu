@@ -109,7 +109,8 @@ static int run_opt(const Index* ix, const void* q, uint64_t m, void* out, cudaSt
 }
 
 template <class K>
-static int run_kary(const Index* ix, const void* q, uint64_t m, void* out, cudaStream_t s, const bs_launch& L) {
+static int run_kary(const Index* ix, const void* q, uint64_t m, void* out, cudaStream_t s, const bs_launch& L,
+                    const PeerLaunch* pl = nullptr) {
     if (!ix->kary_built) return fail(BS_ERR_UNSUPPORTED, "KARY: index built without K-ary levels (layout.variant != KARY)");
     KaryParams<K> p;
     memset(&p, 0, sizeof p);
@@ -127,6 +128,21 @@ static int run_kary(const Index* ix, const void* q, uint64_t m, void* out, cudaS
     const uint32_t GL = C * ix->kb / 32;
     const bool g1 = (L.kary_mode == 6 || L.kary_mode == 7) && W * ix->kb <= 64 && W * ix->kb >= 8 && C * ix->kb >= 32 &&
                     C * ix->kb <= 256;
+    if (pl && !g1)
+        return fail(BS_ERR_UNSUPPORTED, "bs_lookup_peer: needs the thread-per-lookup K-ary kernel (kary_mode 6/7, "
+                                        "W*key <= 64 B, C*key in 32..256 B)");
+    if (pl) {
+        p.peer_cursor = pl->cursor;
+        p.peer_wait = pl->wait;
+        p.peer_wait_target = pl->target;
+        p.peer_tag = pl->tag;
+        p.peer_ret = pl->ret;
+        p.peer_sig = pl->sig;
+        p.peer_done = pl->done;
+        p.peer_err = pl->err;
+        p.peer_base = pl->base;
+        p.peer_P = pl->P;
+    }
     const bool tiered = !g1 && L.kary_mode >= 2 && C >= W && (C / W == 1 || C / W == 2 || C / W == 4);
     const bool pair64 = (L.kary_mode == 3 || L.kary_mode == 5) && ix->kb == 8;
     const bool pipe = L.kary_mode >= 4;   // 4/5: experimental software-pipelined 2/3
@@ -177,7 +193,8 @@ static int run_kary(const Index* ix, const void* q, uint64_t m, void* out, cudaS
         // nreg: low 4 bits = leaf waves in flight IL (default 4), bits 4.. = lookups
         // per thread T (1 or 2, default 1)
         const uint32_t IL = (L.nreg & 15) ? (L.nreg & 15) : 4;
-        const uint32_t T = (L.nreg >> 4) ? (L.nreg >> 4) : 1;
+        uint32_t T = (L.nreg >> 4) ? (L.nreg >> 4) : 1;
+        if (pl && T > 2) T = 2;   // the pipelined FLAT kernel has no peer epilogue
         cudaError_t e = launch_kary_g1(ix->kb, ix->ob, &p, q, m, out, threads, W, GL, IL, T, flat, g, p.smem_bytes, s, &uns);
         if (uns) return fail(BS_ERR_UNSUPPORTED, "KARY g1: threads=%u W=%u C=%u not supported", threads, W, C);
         if (e != cudaSuccess) return fail_cuda(e, "KARY g1 launch");
@@ -229,6 +246,13 @@ static int run_kary(const Index* ix, const void* q, uint64_t m, void* out, cudaS
     if (uns) return fail(BS_ERR_UNSUPPORTED, "KARY: threads=%u waves=%u W=%u not supported", threads, R, ix->kW);
     if (e != cudaSuccess) return fail_cuda(e, "KARY launch");
     return BS_OK;
+}
+
+int dispatch_kary_peer(const Index* ix, const void* q, uint64_t cap, cudaStream_t s, const bs_launch& L,
+                       const PeerLaunch& pl) {
+    if (L.variant != BS_VARIANT_KARY) return fail(BS_ERR_UNSUPPORTED, "bs_lookup_peer: needs variant KARY");
+    return ix->kb == 8 ? run_kary<uint64_t>(ix, q, cap, nullptr, s, L, &pl)
+                       : run_kary<uint32_t>(ix, q, cap, nullptr, s, L, &pl);
 }
 
 int dispatch_lookup(const Index* ix, const void* q, uint64_t m, void* out, cudaStream_t s, const bs_launch& L) {

@@ -57,6 +57,24 @@ struct KaryParams {
     const uint32_t* flat;    // staged from here (2^flat_D words; slot 0 unused)
     const uint64_t* flat64;  // exact u64 copy (tie redo), u64 keys only
     uint32_t flat_D;
+    // fused peer-memory routing (peer.cu, bs_lookup_peer; g1 kernels only).
+    // peer_cursor == nullptr: a plain lookup.  Otherwise the kernel first waits
+    // until *peer_wait >= peer_wait_target (every rank has routed its queries
+    // into this rank's receive window), looks up min(m, *peer_cursor) slots,
+    // and stores each result (global rank = peer_base + local lb, miss bit
+    // kept) straight into the source rank's return window, slot
+    // peer_tag[o] = (src_rank << 32) | src_idx.  The last CTA to finish zeroes
+    // the cursor and bumps every rank's return counter (*peer_sig[r]).
+    unsigned long long* peer_cursor;
+    const unsigned long long* peer_wait;
+    unsigned long long peer_wait_target;
+    const uint64_t* peer_tag;
+    uint64_t* const* peer_ret;             // [P] return windows (peer pointers)
+    unsigned long long* const* peer_sig;   // [P] return-done counters (peer pointers)
+    unsigned int* peer_done;               // local CTA completion counter
+    unsigned int* peer_err;                // local error bits (peer_sync.cuh)
+    uint64_t peer_base;
+    uint32_t peer_P;
 };
 
 // ---- launchers (return cudaGetLastError() after the launch) ----

@@ -1,0 +1,149 @@
+"""bs_build_peer / bs_lookup_peer (fused peer-memory routing, include/bs.h;
+SURVEY §8f f1): bit-exact vs the oracle on the concatenated array.
+
+* world = 1: the route kernel stores every query into the rank's own window,
+  the K-ary kernel's peer epilogue stores every result into its own return
+  window; consecutive calls exercise the monotonic counters.
+* world = 2 on ONE GPU: two processes, each with its own window, mapped into
+  the other with CUDA IPC — the same code path as two GPUs over NVLink, with a
+  run of duplicates straddling the shard boundary (first-occurrence routing).
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import oracle
+import workload
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2506_01576_b200 as P  # noqa: E402
+from paper_2506_01576_b200 import bs  # noqa: E402
+
+
+def _layout(kb):
+    return bs.bs_layout_default(key_bytes=kb, out_bytes=8, variant=bs.KARY)
+
+
+@pytest.mark.parametrize("kb", [8, 4])
+def test_peer_world1(kb):
+    keys = workload.gen_keys(200003, kb, seed=21)
+    idx = bs.bs_build_peer(P.as_torch(keys), keys.size, _layout(kb), 0, 1, 300000)
+    bs.bs_peer_connect(idx, [bs.bs_peer_export(idx)])
+    out = torch.empty(300000, dtype=torch.int64, device="cuda")
+    for call, (m, hr) in enumerate([(300000, 0.6), (0, 1.0), (1, 0.0), (12345, 1.0), (299999, 0.3)]):
+        q = workload.gen_queries(keys, max(m, 1), seed=100 + call, hit_ratio=hr)[:m]
+        dq = P.as_torch(q) if m else None
+        bs.bs_lookup_peer(idx, dq, m, out)
+        torch.cuda.synchronize()
+        if m:
+            got = P.to_numpy_unsigned(out[:m], 8)
+            want = oracle.lookup(keys, q, out_bytes=8)
+            assert np.array_equal(got, want), f"call {call}: first mismatch at {np.flatnonzero(got != want)[:5]}"
+    err, calls = bs.bs_peer_status(idx)
+    assert err == 0 and calls == 5
+    idx.close()
+
+
+def test_peer_overflow_flagged():
+    keys = workload.gen_keys(5000, 8, seed=3)
+    idx = bs.bs_build_peer(P.as_torch(keys), keys.size, _layout(8), 0, 1, 1000, recv_capacity=100)
+    bs.bs_peer_connect(idx, [bs.bs_peer_export(idx)])
+    q = workload.gen_queries(keys, 1000, seed=4)
+    out = torch.empty(1000, dtype=torch.int64, device="cuda")
+    bs.bs_lookup_peer(idx, P.as_torch(q), 1000, out)
+    torch.cuda.synchronize()
+    err, _ = bs.bs_peer_status(idx)
+    assert err & 1
+    idx.close()
+
+
+def test_peer_connect_checks_order():
+    a = workload.gen_keys(1000, 8, seed=5)
+    lo, hi = a[:500], a[500:]
+    i0 = bs.bs_build_peer(P.as_torch(hi), hi.size, _layout(8), 0, 2, 10)
+    i1 = bs.bs_build_peer(P.as_torch(lo), lo.size, _layout(8), 1, 2, 10)
+    with pytest.raises(bs.BsError) as e:
+        bs.bs_peer_connect(i0, [bs.bs_peer_export(i0), bs.bs_peer_export(i1)])
+    assert e.value.code == -6
+    with pytest.raises(bs.BsError):   # rank mismatch in the blob order
+        bs.bs_peer_connect(i0, [bs.bs_peer_export(i1), bs.bs_peer_export(i0)])
+    with pytest.raises(bs.BsError):   # not KARY
+        bs.bs_build_peer(P.as_torch(lo), lo.size, bs.bs_layout_default(key_bytes=8, out_bytes=8, variant=bs.OPT),
+                         0, 1, 10)
+    i0.close()
+    i1.close()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _world2_worker(rank, world, port, keys, cut, calls, ret):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    shard = keys[:cut] if rank == 0 else keys[cut:]
+    max_m = max(m for m, _ in calls)
+    idx = bs.bs_build_peer(P.as_torch(shard), shard.size, _layout(8), rank, world, max_m)
+    bs.bs_peer_connect_group(idx)
+    out = torch.empty(max_m, dtype=torch.int64, device="cuda")
+    res = []
+    for c, (m, hr) in enumerate(calls):
+        q = workload.gen_queries(keys, max(m, 1), seed=1000 * rank + c, hit_ratio=hr)[:m]
+        bs.bs_lookup_peer(idx, P.as_torch(q) if m else None, m, out)
+        torch.cuda.synchronize()
+        got = P.to_numpy_unsigned(out[:m], 8).copy()
+        res.append(bool(np.array_equal(got, oracle.lookup(keys, q, out_bytes=8))))
+    err, _ = bs.bs_peer_status(idx)
+    dist.barrier()
+    idx.close()
+    ret[rank] = (res, err)
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(600)
+def test_peer_world2_one_gpu():
+    import torch.multiprocessing as mp
+    keys = workload.gen_keys(300000, 8, seed=31)
+    cut = 150000
+    keys[cut - 3:cut + 3] = keys[cut - 3]   # duplicates straddling the boundary (still ascending)
+    keys = np.sort(keys)
+    calls = [(200000, 0.7), (0, 1.0), (77777, 1.0), (200000, 0.2)]
+    ctx = mp.get_context("spawn")
+    mgr = ctx.Manager()
+    ret = mgr.dict()
+    mp.start_processes(_world2_worker, args=(2, _free_port(), keys, cut, calls, ret), nprocs=2, join=True,
+                       start_method="spawn")
+    for r in range(2):
+        res, err = ret[r]
+        assert err == 0, f"rank {r}: peer error bits {err}"
+        assert all(res), f"rank {r}: per-call parity {res}"
+
+
+class _DeviceWindow:
+    """Zero-copy torch view of a raw device address (CUDA array interface)."""
+
+    def __init__(self, ptr, n):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<i8", "data": (ptr, False), "version": 3}
+
+
+def test_peer_results_window():
+    keys = workload.gen_keys(70001, 8, seed=41)
+    idx = bs.bs_build_peer(P.as_torch(keys), keys.size, _layout(8), 0, 1, 50000)
+    bs.bs_peer_connect(idx, [bs.bs_peer_export(idx)])
+    q = workload.gen_queries(keys, 50000, seed=42, hit_ratio=0.5)
+    bs.bs_lookup_peer(idx, P.as_torch(q), q.size, None)
+    torch.cuda.synchronize()
+    win = torch.as_tensor(_DeviceWindow(bs.bs_peer_results(idx), q.size), device="cuda")
+    got = P.to_numpy_unsigned(win, 8)
+    assert np.array_equal(got, oracle.lookup(keys, q, out_bytes=8))
+    idx.close()
