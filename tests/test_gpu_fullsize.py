@@ -1,5 +1,6 @@
 """Parity at BASELINE.json's full sizes, in the launch configuration bench.py
-times (configs[1] and configs[2]: 2^20 u32 / 2^26 u64 keys, 2^27 queries).
+times (configs[1], configs[2] and configs[3] per GPU: 2^20 u32 / 2^26 u64 /
+2^30 u64 keys, 2^27 queries; config 3 also in pre-sorted query order).
 
 The oracle cannot run 2^27 bisections in a test's time budget, so (③):
   * a deterministic sample of 2^16 outputs is compared with oracle.lookup
@@ -47,10 +48,11 @@ def _check_invariant(dk, dq, out, n, kb):
     assert bool((hit == ~miss).all()), "hit bit wrong"
 
 
-@pytest.mark.parametrize("cfg", ["config2", "config3"])
-def test_fullsize_bench_launch(cfg):
+@pytest.mark.parametrize("cfg,order", [("config2", "random"), ("config3", "random"), ("config3", "sorted"),
+                                       ("config4", "random")])
+def test_fullsize_bench_launch(cfg, order):
     n, kb, m, hr, _ = bench.CONFIGS[cfg]
-    keys, q, _ = bench.make_inputs(cfg, "random", 0)
+    keys, q, _ = bench.make_inputs(cfg, order, 0)
     dk, dq = P.as_torch(keys), P.as_torch(q)
     out = torch.empty(m, dtype={4: torch.int32, 8: torch.int64}[kb], device="cuda")
     # bench.py's launch configuration: the layout defaults (K, C, kary_mode, threads, nreg)
@@ -64,3 +66,5 @@ def test_fullsize_bench_launch(cfg):
     assert np.array_equal(got, want)
     _check_invariant(dk, dq, out, n, kb)
     idx.close()
+    del dk, dq, out
+    torch.cuda.empty_cache()
