@@ -11,9 +11,9 @@
 //    feeding §5's K-ary levels; D probes, no per-level bookkeeping.
 //  * shared-memory levels: ONE thread per lookup, binary search inside each
 //    node over the image's hi-word plane only (u64; u32 keys are exact).  A
-//    hi-word tie sets a flag and the warp redoes those levels exactly from
-//    the global separator copy (rare for distinct keys, correct always).  With
-//    the lo plane out of shared memory, twice as many levels fit (227 KB).
+//    lane whose query ties a separator's hi word redoes the shared levels
+//    exactly from the global separator copy (only the tied lanes; at small n
+//    a hit query equals a leaf maximum 1 time in C).  With the lo plane out of shared memory, twice as many levels fit.
 //  * global separator levels: still ONE thread per lookup — a node of
 //    W*key <= 64 B is one or two 256-bit loads (sm_100 LDG.E.ENL2.256) by the
 //    owning thread, so a level costs ~17 instructions per 32 lookups and no
@@ -90,15 +90,6 @@ k_kary_g1(const KaryParams<K> p, const K* __restrict__ q, uint64_t m_arg, void* 
         const uint64_t i = t * 32 + lane;
         return (t < nwt && i < m) ? load_stream(q + i, sh, pol_first) : KeyMax<K>::v;
     };
-    // exact in-node rank from the global separator copy (tie redo only)
-    auto node_rank_global = [&](uint32_t l, uint32_t node, K key) -> uint32_t {
-        const K* nd = p.sep + p.lvl_base[l] + (uint64_t)node * W;
-        uint32_t c = 0;
-#pragma unroll
-        for (int s = W / 2; s >= 1; s >>= 1) c += (ld_na(nd + c + s - 1) < key) ? (uint32_t)s : 0u;
-        if (extra) c += (ld_na(nd + c) < key) ? 1u : 0u;
-        return c;
-    };
 
     // T warp-tiles per iteration: each thread carries T independent lookups
     // through the shared and global levels (T loads in flight per thread)
@@ -165,14 +156,24 @@ k_kary_g1(const KaryParams<K> p, const K* __restrict__ q, uint64_t m_arg, void* 
                 node[t] = child < last ? child : last;
             }
         }
-        if (__any_sync(0xFFFFFFFFu, tie)) {
+        if constexpr (sizeof(K) == 8) {
+            // a hi-word tie (q equals a separator's top half: ~1 in C per lookup
+            // at the leaf-max level of a small index): the tied lanes alone redo
+            // the shared levels exactly from the global separator copy
+            if (__any_sync(0xFFFFFFFFu, tie) && tie) {
 #pragma unroll 1
-            for (int t = 0; t < T; ++t) {
-                node[t] = 0;
-                for (uint32_t l = 0; l < Ls; ++l) {
-                    const uint32_t child = node[t] * K_ + node_rank_global(l, node[t], key[t]);
-                    const uint32_t last = p.nodes_next[l] - 1;
-                    node[t] = child < last ? child : last;
+                for (int t = 0; t < T; ++t) {
+                    node[t] = 0;
+#pragma unroll 1
+                    for (uint32_t l = 0; l < Ls; ++l) {
+                        const K* nd = p.sep + p.lvl_base[l] + (uint64_t)node[t] * W;
+                        uint32_t c = 0;
+#pragma unroll
+                        for (int v = 0; v < W; ++v) c += (ldg(nd + v) < key[t]) ? 1u : 0u;
+                        const uint32_t child = node[t] * K_ + c;
+                        const uint32_t last = p.nodes_next[l] - 1;
+                        node[t] = child < last ? child : last;
+                    }
                 }
             }
         }

@@ -5,13 +5,16 @@ python tools/size_sweep.py --kb 4 --lo 15 --hi 29 > gpurun_out/size_sweep.jsonl
 For each n = 2^lo .. 2^hi (step 2): m = 2^27 uniform random hit queries; the
 naive kernel (Listing 1), the OPT kernel (static + steps-pinning, 512 x 4) and
 the K-ary bench kernel (mode 6) — each checked on a sample against the oracle.
-Lines: {"n", "variant", "ms", "G_lookups_per_s", "build_ms", "footprint_bytes", "ok"}.
+Lines: {"n", "variant", "ms", "G_lookups_per_s", "build_ms_sorted_input",
+"build_ms_unsorted_input", "footprint_bytes", "ok"}; build times are host wall
+times of the synchronous bs_build (median of 3 after a warm-up build).
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import time
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -60,6 +63,7 @@ def main():
         keys = workload.gen_keys(n, kb)
         q = workload.gen_queries(keys, m)
         dk, dq = P.as_torch(keys), P.as_torch(q)
+        dk_perm = dk[torch.randperm(n, device="cuda")]
         samp = np.random.default_rng(lg).integers(0, m, size=1 << 12)
         want = oracle.lookup(keys, q[samp], out_bytes=kb)
         runs = [("naive", dict(variant=bs.NAIVE), dict(variant=bs.NAIVE, threads=256)),
@@ -67,6 +71,20 @@ def main():
                                                    reorder=0, schedule=bs.STATIC)),
                 ("kary", dict(variant=bs.KARY, k=a.k, leaf_chunk=a.c), dict(variant=bs.KARY, kary_mode=6))]
         for name, lay_kw, launch_kw in runs:
+            # build time (Fig. 13 analogue): host wall time of the synchronous
+            # bs_build, median of 3 after one warm-up build; input already
+            # sorted (copy + check + auxiliary levels) and unsorted (+ radix sort)
+            bt = {}
+            for srt in (1, 0):
+                ts = []
+                for r in range(4):
+                    lay = bs.bs_layout_default(key_bytes=kb, out_bytes=kb, input_sorted=srt, **lay_kw)
+                    torch.cuda.synchronize()
+                    t0 = time.perf_counter()
+                    ib = bs.bs_build(dk if srt else dk_perm, n, lay)
+                    ts.append((time.perf_counter() - t0) * 1e3)
+                    ib.close()
+                bt[srt] = float(np.median(ts[1:]))
             idx = bs.bs_build(dk, n, bs.bs_layout_default(key_bytes=kb, out_bytes=kb, **lay_kw))
             info = idx.info
 
@@ -75,11 +93,12 @@ def main():
             ms = time_launch(fn, 2, 3)
             ok = bool(np.array_equal(P.to_numpy_unsigned(out, kb)[samp], want))
             print(json.dumps({"n": n, "log2n": lg, "key_bytes": kb, "variant": name, "ms": ms,
-                              "G_lookups_per_s": m / ms / 1e6, "build_ms": info["build_ms"],
+                              "G_lookups_per_s": m / ms / 1e6, "build_ms_sorted_input": bt[1],
+                              "build_ms_unsorted_input": bt[0],
                               "footprint_bytes": info["footprint_bytes"], "array_bytes": info["array_bytes"],
                               "ok": ok}), flush=True)
             idx.close()
-        del dk, dq
+        del dk, dq, dk_perm
         torch.cuda.empty_cache()
 
 
