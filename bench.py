@@ -190,7 +190,7 @@ def main():
     ap.add_argument("--nreg", type=int, default=0)
     ap.add_argument("--reorder", type=int, default=0)
     ap.add_argument("--schedule", type=int, default=1)
-    ap.add_argument("--hints", type=int, default=3)
+    ap.add_argument("--hints", type=int, default=0x100, help="cache_hints bits; 256 = BS_HINT_AUTO (resolved at build)")
     ap.add_argument("--kary-mode", type=int, default=6, help="0 warp, 1 hybrid, 2-5 tiered, 6 thread-per-lookup, 7 + flat table")
     ap.add_argument("--no-naive", action="store_true", help="skip the naive comparison leg")
     ap.add_argument("--no-e2e", action="store_true")
@@ -317,6 +317,7 @@ def main():
         "config": {"workload": f"{args.config}: {desc}", "order": args.order, "variant": args.variant,
                    "k": info["k"], "leaf_chunk": info["leaf_chunk"], "kary_levels": info["kary_levels"],
                    "kary_smem_levels": info["kary_smem_levels"], "queries_per_gpu": m,
+                   "cache_hints": bs.bs_launch_default(idx).cache_hints,
                    "parallelism": f"replicated x{world}" if world > 1 else "1 GPU",
                    "l2": "inputs larger than L2 (queries+results 2 GiB per step > 126 MB), no flush"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,

@@ -107,6 +107,10 @@ typedef struct {
 #define BS_HINT_STREAM_EVICT_FIRST 1u  /* query loads / result stores: L2 evict_first    */
 #define BS_HINT_LEAF_EVICT_FIRST 2u    /* deepest probes / K-ary leaves: L2 evict_first  */
 #define BS_HINT_SEP_EVICT_LAST 4u      /* K-ary separator levels in global memory: L2 evict_last */
+/* Resolved by bs_build (the layout default): STREAM | SEP, plus LEAF when the
+ * sorted array exceeds twice the L2 — evict_first on leaves pays only when
+ * they cannot stay resident (measured: profiles/r1s3f_hints_*.jsonl). */
+#define BS_HINT_AUTO 0x100u
 
 /* Per-call launch override (bs_lookup_ex).  Only launch knobs; the structure
  * built by bs_build (pinned table size, K, C) is fixed.  Field meaning as in

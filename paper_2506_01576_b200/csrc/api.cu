@@ -235,7 +235,7 @@ int bs_layout_default(bs_layout* l) {
     l->k = 5;
     l->leaf_chunk = 16;
     l->ctas_per_sm = 0;
-    l->cache_hints = BS_HINT_STREAM_EVICT_FIRST | BS_HINT_LEAF_EVICT_FIRST;
+    l->cache_hints = BS_HINT_AUTO;
     l->kary_mode = 6;
     return BS_OK;
 }
@@ -285,6 +285,11 @@ int bs_build(const void* keys, uint64_t n, const bs_layout* layout_in, void** ou
         cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, ix->device); ix->smem_optin = v;
         cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerMultiprocessor, ix->device); ix->smem_per_sm = v;
         cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, ix->device); ix->l2_bytes = v;
+    }
+    if (ix->layout.cache_hints & BS_HINT_AUTO) {
+        const uint64_t l2 = ix->l2_bytes ? (uint64_t)ix->l2_bytes : (126ull << 20);
+        ix->layout.cache_hints = BS_HINT_STREAM_EVICT_FIRST | BS_HINT_SEP_EVICT_LAST |
+                                 ((uint64_t)abytes > 2 * l2 ? BS_HINT_LEAF_EVICT_FIRST : 0u);
     }
     e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
     if (e != cudaSuccess) { rc = fail_cuda(e, "cudaStreamCreate"); goto done; }

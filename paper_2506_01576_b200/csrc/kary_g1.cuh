@@ -45,7 +45,7 @@ __device__ __forceinline__ void ld_node(const K* p, bool hint, uint64_t pol, K* 
 }
 
 template <class K, int W, int GL, int IL, int T, bool FLAT>
-__global__ void __launch_bounds__(1024, 1)
+__global__ void __launch_bounds__(T >= 2 ? 768 : 1024, 1)
 k_kary_g1(const KaryParams<K> p, const K* __restrict__ q, uint64_t m_arg, void* __restrict__ out, uint32_t ob) {
     constexpr int VL = 32 / (int)sizeof(K);     // leaf keys per lane (one 256-bit load)
     constexpr int GPWL = 32 / GL;               // leaf lookups per wave
