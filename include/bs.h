@@ -233,6 +233,18 @@ int bs_index_info(const void* idx, bs_info* info);
  * BS_ERR_INVALID if cap is too small, BS_ERR_UNSUPPORTED if not built. */
 int bs_export(const void* idx, int what, void* dst, uint64_t cap, uint64_t* written);
 
+/* Batch insert (the paper's outlook, gives no method):
+ * builds a NEW index, same layout, over the multiset union of idx's keys and
+ * delta_keys (m device keys of idx's key width; delta_sorted = 1 if already
+ * ascending, else the library radix-sorts a copy).  The old array and the
+ * sorted delta are merged on the device (merge path), then the auxiliary
+ * levels are rebuilt.  idx is untouched (destroy it when no lookup on it is in
+ * flight); results on *out_idx follow the result contract over the merged
+ * array.  Synchronous.  m = 0 clones idx.  Errors: BS_ERR_INVALID,
+ * BS_ERR_UNSUPPORTED (multi-GPU index), BS_ERR_NOT_SORTED (delta_sorted = 1
+ * but not ascending), BS_ERR_CUDA / BS_ERR_OOM. */
+int bs_merge(const void* idx, const void* delta_keys, uint64_t m, int delta_sorted, void** out_idx);
+
 /* Library version / build string (arch, commit-independent). */
 const char* bs_version(void);
 

@@ -102,10 +102,11 @@ def lib():
         L.bs_lookup_peer.argtypes = [vp, vp, _u64, vp, vp]
         L.bs_peer_status.argtypes = [vp, ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(_u64)]
         L.bs_peer_results.argtypes = [vp, ctypes.POINTER(vp)]
+        L.bs_merge.argtypes = [vp, vp, _u64, i, ctypes.POINTER(vp)]
         for f in ("bs_layout_default", "bs_launch_default", "bs_build", "bs_lookup", "bs_lookup_ex",
                   "bs_lookup_host", "bs_index_info", "bs_export", "bs_dist_get_uid", "bs_dist_init",
                   "bs_build_dist", "bs_lookup_dist", "bs_build_peer", "bs_peer_export", "bs_peer_connect",
-                  "bs_lookup_peer", "bs_peer_status", "bs_peer_results"):
+                  "bs_lookup_peer", "bs_peer_status", "bs_peer_results", "bs_merge"):
             getattr(L, f).restype = i
         _lib = L
     return _lib
@@ -213,6 +214,13 @@ def bs_lookup_ex(index: Index, queries, m: int, out, stream=None, launch: bs_lau
 
 def bs_lookup_host(index: Index, host_queries, m: int, host_out, stream=None):
     return _check(lib().bs_lookup_host(index.handle, _ptr(host_queries), m, _ptr(host_out), _stream_ptr(stream)))
+
+
+def bs_merge(index: Index, delta_keys, m: int, delta_sorted: bool = False) -> Index:
+    """New index over index's keys plus m delta keys (device), same layout."""
+    h = ctypes.c_void_p()
+    _check(lib().bs_merge(index.handle, _ptr(delta_keys), m, 1 if delta_sorted else 0, ctypes.byref(h)))
+    return Index(h.value, index.layout)
 
 
 def bs_destroy(index: Index):

@@ -43,6 +43,8 @@ static uint32_t pow2_at_least(uint32_t x) {
     return w;
 }
 
+thread_local const void* t_adopt_keys = nullptr;
+
 static void free_index(Index* ix) {
     if (!ix) return;
     if (ix->d_keys) cudaFree(ix->d_keys);
@@ -265,6 +267,9 @@ int bs_build(const void* keys, uint64_t n, const bs_layout* layout_in, void** ou
     if (!reserved_zero(lay.reserved, 6)) return fail(BS_ERR_INVALID, "layout.reserved must be zero");
     if (lay.threads > 1024 || lay.threads % 32) return fail(BS_ERR_INVALID, "threads must be a multiple of 32 <= 1024");
 
+    // bs_merge hands over its merged buffer (allocated with the padding below)
+    const bool adopt = t_adopt_keys != nullptr && t_adopt_keys == keys && lay.input_sorted;
+    t_adopt_keys = nullptr;
     Index* ix = new Index();
     ix->layout = lay;
     ix->n = n;
@@ -286,6 +291,7 @@ int bs_build(const void* keys, uint64_t n, const bs_layout* layout_in, void** ou
         cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerMultiprocessor, ix->device); ix->smem_per_sm = v;
         cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, ix->device); ix->l2_bytes = v;
     }
+    ix->hints_requested = ix->layout.cache_hints;
     if (ix->layout.cache_hints & BS_HINT_AUTO) {
         const uint64_t l2 = ix->l2_bytes ? (uint64_t)ix->l2_bytes : (126ull << 20);
         ix->layout.cache_hints = BS_HINT_STREAM_EVICT_FIRST | BS_HINT_SEP_EVICT_LAST |
@@ -299,8 +305,12 @@ int bs_build(const void* keys, uint64_t n, const bs_layout* layout_in, void** ou
 
     // ---- the sorted array ----
     // +256 keys of MAX padding: leaf chunks (C <= 256) may be read whole with vector loads
-    e = cudaMalloc(&ix->d_keys, abytes + 256 * ix->kb + 16);
-    if (e != cudaSuccess) { rc = fail_cuda(e, "cudaMalloc(keys)"); goto done; }
+    if (adopt) {
+        ix->d_keys = const_cast<void*>(keys);   // bs_merge's merged buffer: owned by the index from here on
+    } else {
+        e = cudaMalloc(&ix->d_keys, abytes + 256 * ix->kb + 16);
+        if (e != cudaSuccess) { rc = fail_cuda(e, "cudaMalloc(keys)"); goto done; }
+    }
     e = cudaMemsetAsync((char*)ix->d_keys + abytes, 0xFF, 256 * ix->kb + 16, st);
     if (e != cudaSuccess) { rc = fail_cuda(e, "memset(pad)"); goto done; }
     {
@@ -309,8 +319,10 @@ int bs_build(const void* keys, uint64_t n, const bs_layout* layout_in, void** ou
                          (pa.type == cudaMemoryTypeDevice || pa.type == cudaMemoryTypeManaged);
         cudaGetLastError();
         if (lay.input_sorted) {
-            e = cudaMemcpyAsync(ix->d_keys, keys, abytes, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st);
-            if (e != cudaSuccess) { rc = fail_cuda(e, "copy keys"); goto done; }
+            if (!adopt) {
+                e = cudaMemcpyAsync(ix->d_keys, keys, abytes, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st);
+                if (e != cudaSuccess) { rc = fail_cuda(e, "copy keys"); goto done; }
+            }
             e = cudaMallocAsync((void**)&d_flag, sizeof(int), st);
             if (e != cudaSuccess) { rc = fail_cuda(e, "cudaMalloc(flag)"); goto done; }
             cudaMemsetAsync(d_flag, 0, sizeof(int), st);

@@ -31,6 +31,7 @@ struct PeerLaunch {
 
 struct Index {
     bs_layout layout{};
+    uint32_t hints_requested = 0;    // layout.cache_hints as given (BS_HINT_AUTO before resolution)
     int device = 0;
     uint32_t kb = 8, ob = 8;
     uint64_t n = 0;
@@ -92,6 +93,10 @@ struct Index {
 };
 
 int fail(int code, const char* fmt, ...);
+// set by bs_merge right before bs_build(merged, ...): the index adopts that
+// device buffer (n keys + 256 keys of padding + 16 B) instead of copying it;
+// the index owns it from then on, on success and on failure alike
+extern thread_local const void* t_adopt_keys;
 int fail_cuda(cudaError_t e, const char* what);
 void table_prefix(const Index* ix, uint64_t entries, bool partial, uint32_t* D, uint32_t* P);
 

@@ -195,8 +195,12 @@ static int run_kary(const Index* ix, const void* q, uint64_t m, void* out, cudaS
         const uint32_t IL = (L.nreg & 15) ? (L.nreg & 15) : 4;
         uint32_t T = (L.nreg >> 4) ? (L.nreg >> 4) : 1;
         if (pl && T > 2) T = 2;   // the pipelined FLAT kernel has no peer epilogue
-        cudaError_t e = launch_kary_g1(ix->kb, ix->ob, &p, q, m, out, threads, W, GL, IL, T, flat, g, p.smem_bytes, s, &uns);
-        if (uns) return fail(BS_ERR_UNSUPPORTED, "KARY g1: threads=%u W=%u C=%u not supported", threads, W, C);
+        // T = 2 carries two lookups per thread in 80 registers: at most 768 threads
+        // (T = 3 is the pipelined FLAT kernel, 1024 threads; without FLAT it runs as T = 2)
+        const bool two = T == 2 || (T >= 3 && !flat);
+        const uint32_t g1_threads = (two && !L.threads) ? 768u : threads;
+        cudaError_t e = launch_kary_g1(ix->kb, ix->ob, &p, q, m, out, g1_threads, W, GL, IL, T, flat, g, p.smem_bytes, s, &uns);
+        if (uns) return fail(BS_ERR_UNSUPPORTED, "KARY g1: threads=%u T=%u W=%u C=%u not supported", g1_threads, T, W, C);
         if (e != cudaSuccess) return fail_cuda(e, "KARY g1 launch");
         return BS_OK;
     }
