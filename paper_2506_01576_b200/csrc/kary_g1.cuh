@@ -44,7 +44,7 @@ __device__ __forceinline__ void ld_node(const K* p, bool hint, uint64_t pol, K* 
     }
 }
 
-template <class K, int W, int GL, int IL, int T, bool FLAT>
+template <class K, int W, int GL, int IL, int T, bool FLAT, bool PEER = false>
 __global__ void __launch_bounds__(T >= 2 ? 768 : 1024, 1)
 k_kary_g1(const KaryParams<K> p, const K* __restrict__ q, uint64_t m_arg, void* __restrict__ out, uint32_t ob) {
     constexpr int VL = 32 / (int)sizeof(K);     // leaf keys per lane (one 256-bit load)
@@ -66,9 +66,9 @@ k_kary_g1(const KaryParams<K> p, const K* __restrict__ q, uint64_t m_arg, void* 
 
     // fused peer routing (bs_lookup_peer): wait until every rank has routed
     // its queries into this rank's window; the slot count is on the device
-    const bool peer = p.peer_cursor != nullptr;
+    constexpr bool peer = PEER;   // PEER instances exist for T = 1 only (go_g1)
     uint64_t m = m_arg;
-    if (peer) {
+    if constexpr (PEER) {
         if (threadIdx.x == 0) peer_wait_ge(p.peer_wait, p.peer_wait_target, p.peer_err);
         __syncthreads();
         const uint64_t got = *(volatile const unsigned long long*)p.peer_cursor;
@@ -104,6 +104,16 @@ k_kary_g1(const KaryParams<K> p, const K* __restrict__ q, uint64_t m_arg, void* 
         for (int t = 0; t < T; ++t) {
             key[t] = key_n[t];
             key_n[t] = load_tile(wt + wstep + t);
+        }
+        // PEER: each owner lane fetches its slot's return tag now; the load is
+        // hidden behind the descent, the leaf epilogue takes it by shuffle
+        uint64_t tag_own[T];
+        if constexpr (PEER) {
+#pragma unroll
+            for (int t = 0; t < T; ++t) {
+                const uint64_t i = (wt + t) * 32 + lane;
+                tag_own[t] = i < m ? __ldcg(p.peer_tag + i) : 0ull;
+            }
         }
         // ---- shared-memory levels: hi words only, exact redo on a tie ----
         uint32_t node[T];
@@ -223,6 +233,8 @@ k_kary_g1(const KaryParams<K> p, const K* __restrict__ q, uint64_t m_arg, void* 
                 const bool last_lt = x[i][VL - 1] < kk[i];
                 lt = group_sum<GL>(lt, gl, fb_leaf);
                 const bool any_eq = (__ballot_sync(0xFFFFFFFFu, eq) & gm) != 0;
+                uint64_t tg = 0;
+                if constexpr (PEER) tg = __shfl_sync(0xFFFFFFFFu, tag_own[t], (b * IL + i) * GPWL + (int)gl);
                 if (jl == GL - 1) {
                     const uint64_t lbv = (uint64_t)cc[i] * C + lt + (last_lt ? 1u : 0u);
                     const bool hit = any_eq && lbv < n;
@@ -230,9 +242,8 @@ k_kary_g1(const KaryParams<K> p, const K* __restrict__ q, uint64_t m_arg, void* 
                     const uint64_t res = hit ? lbv : (lbv | miss);
                     const uint64_t o = (wt + t) * 32 + (uint64_t)((b * IL + i) * GPWL) + gl;
                     if (o < m) {
-                        if (peer) {
+                        if constexpr (PEER) {
                             // result straight into the source rank's return window (P2P store)
-                            const uint64_t tg = __ldcg(p.peer_tag + o);
                             const uint64_t g = lbv + p.peer_base;
                             p.peer_ret[tg >> 32][tg & 0xFFFFFFFFull] = hit ? g : (g | miss);
                         } else if (ob == 8) {
@@ -246,7 +257,7 @@ k_kary_g1(const KaryParams<K> p, const K* __restrict__ q, uint64_t m_arg, void* 
         }
         }
     }
-    if (peer && peer_last_cta(p.peer_done)) {
+    if (PEER && peer_last_cta(p.peer_done)) {
         // every CTA has read the cursor (at its start) and stored its results:
         // re-arm the window, then tell every rank its results have landed
         *p.peer_cursor = 0;
@@ -392,9 +403,12 @@ k_kary_g1p(const KaryParams<K> p, const K* __restrict__ q, uint64_t m, void* __r
 template <class K, int W, int GL, int IL>
 static cudaError_t go_g1(const void* params, const void* q, uint64_t m, void* out, uint32_t ob, uint32_t threads,
                          uint32_t T, bool flat, Grid grid, uint32_t smem, cudaStream_t s, bool* uns) {
+    // bs_lookup_peer fills the peer fields: the PEER instance (T = 1) carries the epilogue
+    const bool peer = ((const KaryParams<K>*)params)->peer_cursor != nullptr;
     auto kern = flat ? (T >= 2 ? k_kary_g1<K, W, GL, IL, 2, true> : k_kary_g1<K, W, GL, IL, 1, true>)
                      : (T >= 2 ? k_kary_g1<K, W, GL, IL, 2, false> : k_kary_g1<K, W, GL, IL, 1, false>);
-    if (flat && T == 3) kern = k_kary_g1p<K, W, GL, IL>;   // T = 3 encodes "pipelined, one lookup per thread"
+    if (peer) kern = flat ? k_kary_g1<K, W, GL, IL, 1, true, true> : k_kary_g1<K, W, GL, IL, 1, false, true>;
+    if (flat && T == 3 && !peer) kern = k_kary_g1p<K, W, GL, IL>;   // T = 3 encodes "pipelined, one lookup per thread"
     cudaFuncAttributes fa;
     cudaError_t e = cudaFuncGetAttributes(&fa, kern);
     if (e != cudaSuccess) return e;

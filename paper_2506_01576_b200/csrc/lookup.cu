@@ -194,7 +194,7 @@ static int run_kary(const Index* ix, const void* q, uint64_t m, void* out, cudaS
         // per thread T (1 or 2, default 1)
         const uint32_t IL = (L.nreg & 15) ? (L.nreg & 15) : 4;
         uint32_t T = (L.nreg >> 4) ? (L.nreg >> 4) : 1;
-        if (pl && T > 2) T = 2;   // the pipelined FLAT kernel has no peer epilogue
+        if (pl) T = 1;   // the peer epilogue is instantiated for one lookup per thread
         // T = 2 carries two lookups per thread in 80 registers: at most 768 threads
         // (T = 3 is the pipelined FLAT kernel, 1024 threads; without FLAT it runs as T = 2)
         const bool two = T == 2 || (T >= 3 && !flat);
