@@ -322,6 +322,9 @@ def main():
                    "l2": "inputs larger than L2 (queries+results 2 GiB per step > 126 MB), no flush"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "traffic_unit": "DRAM bytes per launch (ncu --set full)",
+                     # SURVEY §8d metric (2): the bytes actually touched (ncu) at this run's speed
+                     "traffic_GBps": traffic / (ms_step / 1e3) / 1e9 if traffic else None,
+                     "traffic_frac": traffic / (ms_step / 1e3) / 1e9 / peak if traffic else None,
                      "alg_bytes_per_launch": bpl * m, "bytes_per_lookup_alg": bpl, "peak_source": peak_src},
         "gpu_launches": args.steps,
         "clocks": clocks,
