@@ -52,6 +52,22 @@ def test_merge_parity(kb, variant, m):
     idx.close()
 
 
+@pytest.mark.parametrize("variant", [bs.OPT, bs.KARY])
+def test_merge_u32_out4(variant):
+    keys = workload.gen_keys(30011, 4, seed=71)
+    idx = bs.bs_build(P.as_torch(keys), keys.size, bs.bs_layout_default(key_bytes=4, out_bytes=4, variant=variant))
+    delta = _delta(keys, 9001, seed=72)
+    new = bs.bs_merge(idx, P.as_torch(delta), delta.size)
+    merged_np = np.sort(np.concatenate([keys, delta]))
+    q = np.concatenate([workload.gen_queries(merged_np, 40000, seed=73, hit_ratio=0.5), delta])
+    out = torch.empty(q.size, dtype=torch.int32, device="cuda")
+    bs.bs_lookup(new, P.as_torch(q), q.size, out)
+    torch.cuda.synchronize()
+    assert np.array_equal(P.to_numpy_unsigned(out, 4), oracle.lookup(merged_np, q, out_bytes=4))
+    new.close()
+    idx.close()
+
+
 def test_merge_sorted_delta_flag():
     keys = workload.gen_keys(5000, 8, seed=61)
     idx = bs.bs_build(P.as_torch(keys), keys.size, bs.bs_layout_default(key_bytes=8, out_bytes=8))

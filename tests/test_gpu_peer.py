@@ -86,14 +86,14 @@ def _free_port():
     return p
 
 
-def _world2_worker(rank, world, port, keys, cut, calls, ret):
+def _world2_worker(rank, world, port, keys, cut, calls, ret, kb=8):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.cuda.set_device(0)
     shard = keys[:cut] if rank == 0 else keys[cut:]
     max_m = max(m for m, _ in calls)
-    idx = bs.bs_build_peer(P.as_torch(shard), shard.size, _layout(8), rank, world, max_m)
+    idx = bs.bs_build_peer(P.as_torch(shard), shard.size, _layout(kb), rank, world, max_m)
     bs.bs_peer_connect_group(idx)
     out = torch.empty(max_m, dtype=torch.int64, device="cuda")
     res = []
@@ -111,9 +111,10 @@ def _world2_worker(rank, world, port, keys, cut, calls, ret):
 
 
 @pytest.mark.timeout(600)
-def test_peer_world2_one_gpu():
+@pytest.mark.parametrize("kb", [8, 4])
+def test_peer_world2_one_gpu(kb):
     import torch.multiprocessing as mp
-    keys = workload.gen_keys(300000, 8, seed=31)
+    keys = workload.gen_keys(300000, kb, seed=31)
     cut = 150000
     keys[cut - 3:cut + 3] = keys[cut - 3]   # duplicates straddling the boundary (still ascending)
     keys = np.sort(keys)
@@ -121,7 +122,7 @@ def test_peer_world2_one_gpu():
     ctx = mp.get_context("spawn")
     mgr = ctx.Manager()
     ret = mgr.dict()
-    mp.start_processes(_world2_worker, args=(2, _free_port(), keys, cut, calls, ret), nprocs=2, join=True,
+    mp.start_processes(_world2_worker, args=(2, _free_port(), keys, cut, calls, ret, kb), nprocs=2, join=True,
                        start_method="spawn")
     for r in range(2):
         res, err = ret[r]
