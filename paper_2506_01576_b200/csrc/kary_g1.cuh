@@ -75,9 +75,13 @@ k_kary_g1(const KaryParams<K> p, const K* __restrict__ q, uint64_t m_arg, void* 
         m = got < m_arg ? got : m_arg;
     }
 
-    const uint64_t pol_first = policy_evict_first();
-    const uint64_t pol_last = policy_evict_last();
-    const bool sh = p.stream_hint != 0, lh = p.leaf_hint != 0, sep_last = p.sep_hint != 0;
+    // one instruction form per access: the hint knobs select the POLICY
+    // (evict_normal when off), so no access is issued twice under opposite
+    // predicates (a runtime choice between the hinted and the plain form did)
+    const uint64_t pol_normal = policy_evict_normal();
+    const uint64_t pol_stream = p.stream_hint ? policy_evict_first() : pol_normal;
+    const uint64_t pol_leaf = p.leaf_hint ? policy_evict_first() : pol_normal;
+    const uint64_t pol_sep = p.sep_hint ? policy_evict_last() : pol_normal;
     const uint64_t n = p.n;
     const uint32_t K_ = p.K, C = p.C, L = p.L, Ls = p.Ls;
     const bool extra = (K_ - 1 == (uint32_t)W);
@@ -88,7 +92,7 @@ k_kary_g1(const KaryParams<K> p, const K* __restrict__ q, uint64_t m_arg, void* 
 
     auto load_tile = [&](uint64_t t) -> K {
         const uint64_t i = t * 32 + lane;
-        return (t < nwt && i < m) ? load_stream(q + i, sh, pol_first) : KeyMax<K>::v;
+        return (t < nwt && i < m) ? load_stream(q + i, true, pol_stream) : KeyMax<K>::v;
     };
 
     // T warp-tiles per iteration: each thread carries T independent lookups
@@ -194,7 +198,7 @@ k_kary_g1(const KaryParams<K> p, const K* __restrict__ q, uint64_t m_arg, void* 
             const uint32_t last = p.nodes_next[l] - 1;
             K s[T][W];
 #pragma unroll
-            for (int t = 0; t < T; ++t) ld_node<K, W>(lv + (uint64_t)node[t] * W, sep_last, pol_last, s[t]);
+            for (int t = 0; t < T; ++t) ld_node<K, W>(lv + (uint64_t)node[t] * W, true, pol_sep, s[t]);
 #pragma unroll
             for (int t = 0; t < T; ++t) {
                 uint32_t c = 0;
@@ -217,7 +221,7 @@ k_kary_g1(const KaryParams<K> p, const K* __restrict__ q, uint64_t m_arg, void* 
                 const int src = (b * IL + i) * GPWL + (int)gl;
                 kk[i] = __shfl_sync(0xFFFFFFFFu, key[t], src);
                 cc[i] = __shfl_sync(0xFFFFFFFFu, node[t], src);
-                ldv<K, VL>(p.a + (uint64_t)cc[i] * C + jl * VL, lh, pol_first, x[i]);
+                ldv<K, VL>(p.a + (uint64_t)cc[i] * C + jl * VL, true, pol_leaf, x[i]);
             }
 #pragma unroll
             for (int i = 0; i < IL; ++i) {
@@ -247,9 +251,9 @@ k_kary_g1(const KaryParams<K> p, const K* __restrict__ q, uint64_t m_arg, void* 
                             const uint64_t g = lbv + p.peer_base;
                             p.peer_ret[tg >> 32][tg & 0xFFFFFFFFull] = hit ? g : (g | miss);
                         } else if (ob == 8) {
-                            store_stream((uint64_t*)out + o, res, sh, pol_first);
+                            store_stream((uint64_t*)out + o, res, true, pol_stream);
                         } else {
-                            store_stream((uint32_t*)out + o, (uint32_t)res, sh, pol_first);
+                            store_stream((uint32_t*)out + o, (uint32_t)res, true, pol_stream);
                         }
                     }
                 }
@@ -288,9 +292,13 @@ k_kary_g1p(const KaryParams<K> p, const K* __restrict__ q, uint64_t m, void* __r
 
     stage_image<uint32_t, false>(S, p.flat, 0, 1u << p.flat_D, bar);
 
-    const uint64_t pol_first = policy_evict_first();
-    const uint64_t pol_last = policy_evict_last();
-    const bool sh = p.stream_hint != 0, lh = p.leaf_hint != 0, sep_last = p.sep_hint != 0;
+    // one instruction form per access: the hint knobs select the POLICY
+    // (evict_normal when off), so no access is issued twice under opposite
+    // predicates (a runtime choice between the hinted and the plain form did)
+    const uint64_t pol_normal = policy_evict_normal();
+    const uint64_t pol_stream = p.stream_hint ? policy_evict_first() : pol_normal;
+    const uint64_t pol_leaf = p.leaf_hint ? policy_evict_first() : pol_normal;
+    const uint64_t pol_sep = p.sep_hint ? policy_evict_last() : pol_normal;
     const uint64_t n = p.n;
     const uint32_t K_ = p.K, C = p.C, L = p.L, Ls = p.Ls, D = p.flat_D;
     const uint32_t fb_leaf = bitlen_c(C - 1);
@@ -302,7 +310,7 @@ k_kary_g1p(const KaryParams<K> p, const K* __restrict__ q, uint64_t m, void* __r
 
     auto load_tile = [&](uint64_t t) -> K {
         const uint64_t i = t * 32 + lane;
-        return (t < nwt && i < m) ? load_stream(q + i, sh, pol_first) : KeyMax<K>::v;
+        return (t < nwt && i < m) ? load_stream(q + i, true, pol_stream) : KeyMax<K>::v;
     };
     auto probe = [&](uint32_t& k, K kq, bool& tie) {
         const uint32_t h = S[k];
@@ -342,7 +350,7 @@ k_kary_g1p(const KaryParams<K> p, const K* __restrict__ q, uint64_t m, void* __r
         // ---- global separator levels of tile t, next tile's probes in between ----
         for (uint32_t l = Ls; l < L; ++l) {
             K s[W];
-            ld_node<K, W>(p.sep + p.lvl_base[l] + (uint64_t)node * W, sep_last, pol_last, s);
+            ld_node<K, W>(p.sep + p.lvl_base[l] + (uint64_t)node * W, true, pol_sep, s);
             for (uint32_t r = 0; r < per && dn < D; ++r, ++dn) probe(kn, key_n, tie_n);
             uint32_t c = 0;
 #pragma unroll
@@ -362,7 +370,7 @@ k_kary_g1p(const KaryParams<K> p, const K* __restrict__ q, uint64_t m, void* __r
                 const int src = (b * IL + i) * GPWL + (int)gl;
                 kk[i] = __shfl_sync(0xFFFFFFFFu, key, src);
                 cc[i] = __shfl_sync(0xFFFFFFFFu, node, src);
-                ldv<K, VL>(p.a + (uint64_t)cc[i] * C + jl * VL, lh, pol_first, x[i]);
+                ldv<K, VL>(p.a + (uint64_t)cc[i] * C + jl * VL, true, pol_leaf, x[i]);
             }
             for (; dn < D; ++dn) probe(kn, key_n, tie_n);
 #pragma unroll
@@ -384,8 +392,8 @@ k_kary_g1p(const KaryParams<K> p, const K* __restrict__ q, uint64_t m, void* __r
                     const uint64_t res = hit ? lbv : (lbv | miss);
                     const uint64_t o = wt * 32 + (uint64_t)((b * IL + i) * GPWL) + gl;
                     if (o < m) {
-                        if (ob == 8) store_stream((uint64_t*)out + o, res, sh, pol_first);
-                        else store_stream((uint32_t*)out + o, (uint32_t)res, sh, pol_first);
+                        if (ob == 8) store_stream((uint64_t*)out + o, res, true, pol_stream);
+                        else store_stream((uint32_t*)out + o, (uint32_t)res, true, pol_stream);
                     }
                 }
             }
