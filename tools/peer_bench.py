@@ -2,8 +2,10 @@
 config-3 workload through bs_lookup (no routing), bs_lookup_dist (NCCL:
 route/count/host-sync/all-to-all/unroute) and bs_lookup_peer (fused peer
 stores + device counters).  CUDA events on the launch stream, median of
---reps; one JSON line per path.  Under torchrun (world > 1, one process per
-GPU) every rank holds 2^26/world keys and 2^27/world queries (partitioned).
+--reps (max over ranks); one JSON line per path.  Under torchrun (world > 1, one process per
+GPU) every rank holds 2^26/world keys and 2^27/world queries (partitioned);
+ranks beyond the visible GPUs share them (functional check only, e.g.
+`torchrun --nproc-per-node 2` on a 1-GPU box).
 
 python tools/peer_bench.py [--reps 10] [--m-log2 27] [--n-log2 26]
 """
@@ -49,7 +51,8 @@ def main():
     a = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    # ranks beyond the visible GPUs share them (functional runs on a 1-GPU box)
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")) % torch.cuda.device_count())
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("gloo")
@@ -86,6 +89,12 @@ def main():
     sample = np.arange(0, m, max(1, m // 4096))
     got = P.to_numpy_unsigned(out, 8)[sample]
     ok = bool(np.array_equal(got, oracle.lookup(keys, q[sample], out_bytes=8))) and err == 0
+    if world > 1:   # the job's time is the slowest rank's
+        import torch.distributed as dist
+        t = torch.tensor([ms for _, ms in rows] + [0.0 if ok else 1.0], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        rows = [(name, float(t[i])) for i, (name, _) in enumerate(rows)]
+        ok = ok and float(t[-1]) == 0.0
     if rank == 0:
         for name, ms in rows:
             print(json.dumps({"path": name, "world": world, "n": n, "m_per_rank": m, "ms": ms,
