@@ -343,8 +343,9 @@ int bs_peer_connect(void* idx, const void* blobs);
  * out_local: m_local u64 global results (device pointers, must not overlap
  * the index's windows), or NULL to leave the results in the return window
  * (bs_peer_results; saves one copy, valid until the next call).  A peer that never joins makes the waits time out
- * after 20 s (error bit 2 in bs_peer_status, results undefined) instead of
- * hanging the GPU.  Not thread-safe per index. */
+ * (after BS_PEER_WAIT_MS from the environment at build time, default 20000;
+ * error bit 2 in bs_peer_status, results undefined) instead of hanging the
+ * GPU.  Not thread-safe per index. */
 int bs_lookup_peer(const void* idx, const void* local_queries, uint64_t m_local, void* out_local, void* stream);
 
 /* *results = device pointer of this rank's return window: after a

@@ -25,6 +25,8 @@
 // results cross the fabric exactly once each, with no staging copies.  The
 // monotonic counters make consecutive calls safe without resets (see
 // DESIGN.md §8 for the ordering argument); waits are bounded (peer_sync.cuh).
+#include <cstddef>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -50,7 +52,8 @@ struct PeerDev {
 // control block at the start of each rank's region
 struct PeerCtl {
     unsigned long long route_sig, ret_sig, cursor;
-    unsigned int done_route, done_look, err, pad;
+    unsigned int done_route, done_look, err;
+    unsigned int wait_ms;   // bounded-wait limit, read next to err by peer_wait_ge (peer_sync.cuh)
 };
 
 struct PeerBlob {
@@ -227,6 +230,15 @@ int bs_build_peer(const void* local_keys, uint64_t n_local, const bs_layout* lay
     if (e != cudaSuccess) return cleanup(fail(BS_ERR_OOM, "bs_build_peer: cudaMalloc(%llu B window): %s",
                                               (unsigned long long)d->lay.total, cudaGetErrorString(e)));
     e = cudaMemset(d->region, 0, 256);
+    if (e == cudaSuccess) {
+        // bounded waits: BS_PEER_WAIT_MS (default 20000) before a wait gives up
+        unsigned wait_ms = 20000;
+        if (const char* v = getenv("BS_PEER_WAIT_MS")) {
+            const long x = atol(v);
+            if (x > 0 && x < 3600000) wait_ms = (unsigned)x;
+        }
+        e = cudaMemcpy((char*)d->region + offsetof(PeerCtl, wait_ms), &wait_ms, sizeof wait_ms, cudaMemcpyHostToDevice);
+    }
     if (e == cudaSuccess) e = cudaIpcGetMemHandle(&d->handle, d->region);
     if (e == cudaSuccess) e = cudaMalloc(&d->d_peers, sizeof(PeerDev) * world);
     if (e == cudaSuccess) e = cudaMalloc(&d->d_ret, sizeof(uint64_t*) * world);

@@ -12,7 +12,7 @@ namespace bs {
 
 constexpr unsigned kPeerErrOverflow = 1u;   // a receive window was full (queries dropped)
 constexpr unsigned kPeerErrTimeout = 2u;    // a wait gave up (a peer never signalled)
-constexpr unsigned long long kPeerWaitNs = 20ull * 1000 * 1000 * 1000;   // 20 s
+constexpr unsigned long long kPeerWaitNs = 20ull * 1000 * 1000 * 1000;   // 20 s (default)
 
 __device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
     unsigned long long v;
@@ -31,13 +31,17 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 }
 
 // Spin (one thread) until *p >= target; bounded so a dead peer cannot hang
-// the GPU: after kPeerWaitNs the error bit is set and the wait returns.
+// the GPU: after the limit the error bit is set and the wait returns.  The
+// limit in ms sits in the word after the error bits (PeerCtl::wait_ms; 0 =
+// kPeerWaitNs).
 __device__ __forceinline__ void peer_wait_ge(const unsigned long long* p, unsigned long long target, unsigned* err) {
     if (ld_acquire_sys_u64(p) >= target) return;
+    const unsigned wait_ms = *(volatile unsigned*)(err + 1);
+    const unsigned long long limit = wait_ms ? (unsigned long long)wait_ms * 1000000ull : kPeerWaitNs;
     const unsigned long long t0 = globaltimer_ns();
     while (ld_acquire_sys_u64(p) < target) {
         __nanosleep(500);
-        if (globaltimer_ns() - t0 > kPeerWaitNs) {
+        if (globaltimer_ns() - t0 > limit) {
             atomicOr(err, kPeerErrTimeout);
             return;
         }

@@ -148,3 +148,34 @@ def test_peer_results_window():
     got = P.to_numpy_unsigned(win, 8)
     assert np.array_equal(got, oracle.lookup(keys, q, out_bytes=8))
     idx.close()
+
+
+def _absent_peer_worker(rank, world, port, keys, ret):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), BS_PEER_WAIT_MS="1500")
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    half = keys.size // 2
+    shard = keys[:half] if rank == 0 else keys[half:]
+    idx = bs.bs_build_peer(P.as_torch(shard), shard.size, _layout(8), rank, world, 1000)
+    bs.bs_peer_connect_group(idx)
+    if rank == 0:   # rank 1 never calls: rank 0's waits must give up, not hang the GPU
+        q = workload.gen_queries(keys, 1000, seed=5)
+        out = torch.empty(1000, dtype=torch.int64, device="cuda")
+        bs.bs_lookup_peer(idx, P.as_torch(q), 1000, out)
+        torch.cuda.synchronize()
+        ret[rank] = bs.bs_peer_status(idx)[0]
+    dist.barrier()
+    idx.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_peer_absent_peer_times_out():
+    import torch.multiprocessing as mp
+    keys = workload.gen_keys(20000, 8, seed=81)
+    mgr = mp.get_context("spawn").Manager()
+    ret = mgr.dict()
+    mp.start_processes(_absent_peer_worker, args=(2, _free_port(), keys, ret), nprocs=2, join=True,
+                       start_method="spawn")
+    assert ret[0] & 2, f"expected the timeout bit, got {ret[0]}"
