@@ -191,7 +191,8 @@ def main():
     ap.add_argument("--reorder", type=int, default=0)
     ap.add_argument("--schedule", type=int, default=1)
     ap.add_argument("--hints", type=int, default=0x100, help="cache_hints bits; 256 = BS_HINT_AUTO (resolved at build)")
-    ap.add_argument("--kary-mode", type=int, default=6, help="0 warp, 1 hybrid, 2-5 tiered, 6 thread-per-lookup, 7 + flat table")
+    ap.add_argument("--kary-mode", type=int, default=8,
+                    help="0 warp, 1 hybrid, 2-5 tiered, 6 thread-per-lookup, 7 + flat table, 8 auto (resolved at build)")
     ap.add_argument("--no-naive", action="store_true", help="skip the naive comparison leg")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=1 << 22)
@@ -306,7 +307,7 @@ def main():
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         tj = json.load(open(tp))
-        key = f"{args.config}/{args.order}/{args.variant}/K{K}/C{C}/mode{args.kary_mode}"
+        key = f"{args.config}/{args.order}/{args.variant}/K{K}/C{C}/mode{bs.bs_launch_default(idx).kary_mode}"
         if key in tj:
             traffic = tj[key]["dram_bytes_per_launch"]
     info = idx.info
@@ -318,6 +319,7 @@ def main():
                    "k": info["k"], "leaf_chunk": info["leaf_chunk"], "kary_levels": info["kary_levels"],
                    "kary_smem_levels": info["kary_smem_levels"], "queries_per_gpu": m,
                    "cache_hints": bs.bs_launch_default(idx).cache_hints,
+                   "kary_mode": bs.bs_launch_default(idx).kary_mode,
                    "parallelism": f"replicated x{world}" if world > 1 else "1 GPU",
                    "l2": "inputs larger than L2 (queries+results 2 GiB per step > 126 MB), no flush"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
