@@ -224,12 +224,13 @@ def main():
     out = torch.empty(m, dtype={4: torch.int32, 8: torch.int64}[ob], device="cuda")
 
     K = args.k or 5
-    C = args.leaf_chunk or 16
+    C = args.leaf_chunk   # 0 = auto (resolved at build; config 3 -> 16)
     lay = bs.bs_layout_default(key_bytes=kb, out_bytes=ob, variant=VARIANTS[args.variant], k=K, leaf_chunk=C,
                                schedule=args.schedule, threads=args.threads, nreg=args.nreg,
                                reorder=args.reorder, cache_hints=args.hints,
                                kary_mode=args.kary_mode)
     idx = bs.bs_build(dk, n, lay)
+    C = idx.info["leaf_chunk"]
     del dk
     stream = torch.cuda.Stream()
 

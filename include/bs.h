@@ -82,7 +82,10 @@ typedef struct {
     uint32_t pin_partial;   /* OPT: 1 = "full-pinning" (partial step M+1), 0 = "steps-pinning" */
     uint32_t reorder;       /* bs_reorder (OPT only)                                        */
     uint32_t k;             /* KARY fan-out K, 2..33 (P:223 A6000 best K = 17)       */
-    uint32_t leaf_chunk;    /* KARY leaf chunk C in keys, power of two 1..256       */
+    uint32_t leaf_chunk;    /* KARY leaf chunk C in keys, power of two 1..256; 0 =
+                               auto (layout default), resolved by bs_build: the smallest
+                               leaf of 32/64/128 B whose bottom separator level fits L2/6,
+                               else 128 B (config 3: C = 16; config 2: C = 8)             */
     uint32_t ctas_per_sm;   /* STATIC schedule: resident CTAs per SM; 0 = auto              */
     uint32_t cache_hints;   /* bitmask BS_HINT_*; 0 = plain loads/stores                    */
     uint32_t kary_mode;     /* KARY schedule (same index, same results):

@@ -235,7 +235,7 @@ int bs_layout_default(bs_layout* l) {
     l->pin_partial = 1;
     l->reorder = BS_REORDER_NONE;
     l->k = 5;
-    l->leaf_chunk = 16;
+    l->leaf_chunk = 0;   // auto: resolved by bs_build from the array size
     l->ctas_per_sm = 0;
     l->cache_hints = BS_HINT_AUTO;
     l->kary_mode = BS_KARY_MODE_AUTO;
@@ -263,7 +263,8 @@ int bs_build(const void* keys, uint64_t n, const bs_layout* layout_in, void** ou
     if (lay.reorder > BS_REORDER_FULL) return fail(BS_ERR_INVALID, "unknown reorder %u", lay.reorder);
     if (lay.kary_mode > BS_KARY_MODE_AUTO) return fail(BS_ERR_INVALID, "unknown kary_mode %u", lay.kary_mode);
     if (lay.k < 2 || lay.k > 33) return fail(BS_ERR_INVALID, "K must be in [2, 33]");
-    if (!is_pow2(lay.leaf_chunk) || lay.leaf_chunk > 256) return fail(BS_ERR_INVALID, "leaf_chunk must be a power of two <= 256");
+    if (lay.leaf_chunk != 0 && (!is_pow2(lay.leaf_chunk) || lay.leaf_chunk > 256))
+        return fail(BS_ERR_INVALID, "leaf_chunk must be 0 (auto) or a power of two <= 256");
     if (!reserved_zero(lay.reserved, 6)) return fail(BS_ERR_INVALID, "layout.reserved must be zero");
     if (lay.threads > 1024 || lay.threads % 32) return fail(BS_ERR_INVALID, "threads must be a multiple of 32 <= 1024");
 
@@ -376,6 +377,19 @@ int bs_build(const void* keys, uint64_t n, const bs_layout* layout_in, void** ou
 
     // ---- K-ary separator levels (§5) ----
     ix->kK = lay.k;
+    ix->leaf_chunk_requested = lay.leaf_chunk;
+    if (lay.leaf_chunk == 0) {
+        // the smallest leaf of 32 / 64 / 128 bytes whose bottom separator level
+        // (one key per leaf) stays within L2/6, else one 128-B line: small
+        // arrays read one 32-B sector per lookup, large ones keep the separator
+        // levels L2-resident (measured optima at every size: profiles/r1s3x_*)
+        const uint64_t l2 = ix->l2_bytes ? (uint64_t)ix->l2_bytes : (126ull << 20);
+        uint32_t leaf_bytes = 128;
+        for (uint32_t b = 32; b < 128; b <<= 1)
+            if ((uint64_t)abytes / b * ix->kb <= l2 / 6) { leaf_bytes = b; break; }
+        lay.leaf_chunk = leaf_bytes / ix->kb;
+        ix->layout.leaf_chunk = lay.leaf_chunk;
+    }
     ix->kC = lay.leaf_chunk;
     ix->kW = pow2_at_least(lay.k - 1 < 2 ? 2 : lay.k - 1);
     if (ix->kW > 32) { rc = fail(BS_ERR_INVALID, "K - 1 must be <= 32"); goto done; }

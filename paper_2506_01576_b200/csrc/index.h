@@ -33,6 +33,7 @@ struct Index {
     bs_layout layout{};
     uint32_t hints_requested = 0;    // layout.cache_hints as given (BS_HINT_AUTO before resolution)
     uint32_t kary_mode_requested = 0;  // layout.kary_mode as given (BS_KARY_MODE_AUTO before resolution)
+    uint32_t leaf_chunk_requested = 0; // layout.leaf_chunk as given (0 = auto before resolution)
     int device = 0;
     uint32_t kb = 8, ob = 8;
     uint64_t n = 0;

@@ -68,6 +68,7 @@ int bs_merge(const void* idx, const void* delta_keys, uint64_t m, int delta_sort
     bs_layout lay = ix->layout;
     lay.cache_hints = ix->hints_requested;
     lay.kary_mode = ix->kary_mode_requested;
+    lay.leaf_chunk = ix->leaf_chunk_requested;
     lay.input_sorted = 1;
     const uint64_t total = ix->n + m;
     if (lay.out_bytes == 4 && total >= (1ull << 31)) return fail(BS_ERR_INVALID, "bs_merge: out_bytes = 4 requires n + m < 2^31");

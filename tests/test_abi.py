@@ -35,7 +35,7 @@ def test_layout_default_and_version():
     lay = bs.bs_layout_default()
     assert lay.struct_size == ctypes.sizeof(bs.bs_layout)
     assert lay.key_bytes == 8 and lay.out_bytes == 8
-    assert lay.variant == bs.KARY and lay.k == 5 and lay.leaf_chunk == 16
+    assert lay.variant == bs.KARY and lay.k == 5 and lay.leaf_chunk == 0
     # schedule and L2 hints are resolved by bs_build from the array size (include/bs.h)
     assert lay.kary_mode == 8 and lay.cache_hints == 0x100
     assert "sm_100a" in bs.bs_version()

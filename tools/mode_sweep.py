@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--hi", type=int, default=26)
     ap.add_argument("--step", type=int, default=2)
     ap.add_argument("--modes", default="2,3,6,7")
+    ap.add_argument("--kc", default="5/16", help="K/C pairs, e.g. 5/16,5/8,5/4")
     a = ap.parse_args()
     torch.cuda.set_device(0)
     kb, m = a.kb, 1 << 27
@@ -42,13 +43,15 @@ def main():
         dk, dq = P.as_torch(keys), P.as_torch(q)
         samp = np.random.default_rng(lg).integers(0, m, size=1 << 12)
         want = oracle.lookup(keys, q[samp], out_bytes=kb)
-        idx = bs.bs_build(dk, n, bs.bs_layout_default(key_bytes=kb, out_bytes=kb))
-        for mode in (int(x) for x in a.modes.split(",")):
-            ms = time_launch(lambda: bs.bs_lookup_ex(idx, dq, m, out, None, kary_mode=mode), 2, 3)
-            ok = bool(np.array_equal(P.to_numpy_unsigned(out, kb)[samp], want))
-            print(json.dumps({"log2n": lg, "key_bytes": kb, "kary_mode": mode, "ms": ms,
-                              "G_lookups_per_s": m / ms / 1e6, "ok": ok}), flush=True)
-        idx.close()
+        for kc in a.kc.split(","):
+            K, C = (int(x) for x in kc.split("/"))
+            idx = bs.bs_build(dk, n, bs.bs_layout_default(key_bytes=kb, out_bytes=kb, k=K, leaf_chunk=C))
+            for mode in (int(x) for x in a.modes.split(",")):
+                ms = time_launch(lambda: bs.bs_lookup_ex(idx, dq, m, out, None, kary_mode=mode), 2, 3)
+                ok = bool(np.array_equal(P.to_numpy_unsigned(out, kb)[samp], want))
+                print(json.dumps({"log2n": lg, "key_bytes": kb, "K": K, "C": C, "kary_mode": mode, "ms": ms,
+                                  "G_lookups_per_s": m / ms / 1e6, "ok": ok}), flush=True)
+            idx.close()
         del dk, dq
         torch.cuda.empty_cache()
 

@@ -53,7 +53,7 @@ def main():
     ap.add_argument("--step", type=int, default=2)
     ap.add_argument("--m-log2", type=int, default=27)
     ap.add_argument("--k", type=int, default=5)
-    ap.add_argument("--c", type=int, default=16)
+    ap.add_argument("--c", type=int, default=0, help="leaf chunk; 0 = the layout's auto choice")
     a = ap.parse_args()
     torch.cuda.set_device(0)
     kb, m = a.kb, 1 << a.m_log2
@@ -69,7 +69,7 @@ def main():
         runs = [("naive", dict(variant=bs.NAIVE), dict(variant=bs.NAIVE, threads=256)),
                 ("opt", dict(variant=bs.OPT), dict(variant=bs.OPT, threads=512, nreg=4, use_pinned=1, pin_partial=0,
                                                    reorder=0, schedule=bs.STATIC)),
-                ("kary", dict(variant=bs.KARY, k=a.k, leaf_chunk=a.c), dict(variant=bs.KARY, kary_mode=6))]
+                ("kary", dict(variant=bs.KARY, k=a.k, leaf_chunk=a.c), dict(variant=bs.KARY))]
         for name, lay_kw, launch_kw in runs:
             # build time (Fig. 13 analogue): host wall time of the synchronous
             # bs_build, median of 3 after one warm-up build; input already
@@ -96,6 +96,7 @@ def main():
                               "G_lookups_per_s": m / ms / 1e6, "build_ms_sorted_input": bt[1],
                               "build_ms_unsorted_input": bt[0],
                               "footprint_bytes": info["footprint_bytes"], "array_bytes": info["array_bytes"],
+                              "leaf_chunk": info["leaf_chunk"], "kary_mode": bs.bs_launch_default(idx).kary_mode,
                               "ok": ok}), flush=True)
             idx.close()
         del dk, dq, dk_perm
