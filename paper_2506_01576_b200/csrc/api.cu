@@ -195,6 +195,7 @@ static int build_kary_layout(Index* ix, cudaStream_t st) {
         for (uint32_t l = lt; l < L; ++l) span *= K;
         ix->flat_level = lt;
         ix->flat_M = nl - 1;
+        ix->flat_span = span;
         ix->flat_D = D;
         e = cudaMalloc(&ix->d_flat, 4ull << D);
         if (e != cudaSuccess) return fail_cuda(e, "cudaMalloc(flat table)");

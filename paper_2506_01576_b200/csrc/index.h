@@ -78,6 +78,7 @@ struct Index {
     void* d_flat = nullptr;
     void* d_flat64 = nullptr;
     uint64_t flat_M = 0;             // node maxima stored (nodes - 1)
+    uint64_t flat_span = 0;          // keys under one flat-level node
     uint32_t flat_level = 0, flat_D = 0;   // Eytzinger slots 1..2^flat_D - 1
 
     // device

@@ -11,8 +11,9 @@
 //    feeding §5's K-ary levels; D probes, no per-level bookkeeping.
 //  * shared-memory levels: ONE thread per lookup, binary search inside each
 //    node over the image's hi-word plane only (u64; u32 keys are exact).  A
-//    lane whose query ties a separator's hi word redoes the shared levels
-//    exactly from the global separator copy (only the tied lanes; at small n
+//    lane whose query ties a separator's hi word fixes its node by stepping
+//    over the level's maxima that share q's hi word and are still < q, read
+//    from the sorted array (only the tied lanes, usually one load; at small n
 //    a hit query equals a leaf maximum 1 time in C).  With the lo plane out of shared memory, twice as many levels fit.
 //  * global separator levels: still ONE thread per lookup — a node of
 //    W*key <= 64 B is one or two 256-bit loads (sm_100 LDG.E.ENL2.256) by the
@@ -147,18 +148,28 @@ k_kary_g1(const KaryParams<K> p, const K* __restrict__ q, uint64_t m_arg, void* 
                     k[t] = 2 * k[t] + (less ? 1u : 0u);
                 }
             }
+#pragma unroll
+            for (int t = 0; t < T; ++t) node[t] = k[t] - (1u << D);
             if constexpr (sizeof(K) == 8) {
-                if (__any_sync(0xFFFFFFFFu, tie)) {
+                // hi-word ties: node = #(maxima whose hi word < q's), a lower
+                // bound on the exact count; the tied lanes step over the maxima
+                // that share q's hi word and are still < q — read straight from
+                // the sorted array (max of node c = a[min((c+1)*span, n) - 1]),
+                // usually one load instead of redoing all D levels
+                if (__any_sync(0xFFFFFFFFu, tie) && tie) {
 #pragma unroll 1
                     for (int t = 0; t < T; ++t) {
-                        k[t] = 1;
-                        for (uint32_t d = 0; d < D; ++d)
-                            k[t] = 2 * k[t] + ((ldg(p.flat64 + k[t]) < (uint64_t)key[t]) ? 1u : 0u);
+                        uint64_t c = node[t];
+                        while (c < p.flat_M) {
+                            uint64_t end = (c + 1) * p.flat_span;
+                            if (end > n) end = n;
+                            if (ldg(p.a + end - 1) < (uint64_t)key[t]) ++c;
+                            else break;
+                        }
+                        node[t] = (uint32_t)c;
                     }
                 }
             }
-#pragma unroll
-            for (int t = 0; t < T; ++t) node[t] = k[t] - (1u << D);
         } else {
         for (uint32_t l = 0; l < Ls; ++l) {
             const uint32_t last = p.nodes_next[l] - 1;
@@ -172,22 +183,22 @@ k_kary_g1(const KaryParams<K> p, const K* __restrict__ q, uint64_t m_arg, void* 
         }
         if constexpr (sizeof(K) == 8) {
             // a hi-word tie (q equals a separator's top half: ~1 in C per lookup
-            // at the leaf-max level of a small index): the tied lanes alone redo
-            // the shared levels exactly from the global separator copy
+            // at the leaf-max level of a small index) is fixed by the tied lanes
+            // (the hi-word descent is exact for the hi-word order, so node is
+            // #(level-Ls subtree maxima whose hi word < q's): step the tied
+            // lanes over the maxima that share q's hi word and are still < q,
+            // read from the sorted array — usually one load)
             if (__any_sync(0xFFFFFFFFu, tie) && tie) {
 #pragma unroll 1
                 for (int t = 0; t < T; ++t) {
-                    node[t] = 0;
-#pragma unroll 1
-                    for (uint32_t l = 0; l < Ls; ++l) {
-                        const K* nd = p.sep + p.lvl_base[l] + (uint64_t)node[t] * W;
-                        uint32_t c = 0;
-#pragma unroll
-                        for (int v = 0; v < W; ++v) c += (ldg(nd + v) < key[t]) ? 1u : 0u;
-                        const uint32_t child = node[t] * K_ + c;
-                        const uint32_t last = p.nodes_next[l] - 1;
-                        node[t] = child < last ? child : last;
+                    uint64_t c = node[t];
+                    while (c < p.flat_M) {
+                        uint64_t end = (c + 1) * p.flat_span;
+                        if (end > n) end = n;
+                        if (ldg(p.a + end - 1) < (uint64_t)key[t]) ++c;
+                        else break;
                     }
+                    node[t] = (uint32_t)c;
                 }
             }
         }

@@ -175,6 +175,13 @@ static int run_kary(const Index* ix, const void* q, uint64_t m, void* out, cudaS
                 ++Li;
         }
         p.Ls = Li;
+        // tie fix-up (kary_g1.cuh): node maxima of level Li = a[min((c+1)*span, n) - 1]
+        if (Li > 0) {
+            uint64_t span = ix->kC;
+            for (uint32_t l = Li; l < ix->kL; ++l) span *= ix->kK;
+            p.flat_span = span;
+            p.flat_M = ix->k_next[Li - 1] - 1;
+        }
         p.img = (const uint32_t*)ix->d_img;
         p.img_plane_words = ix->img_base[ix->img_L];
         for (uint32_t l = 0; l < Li; ++l) p.img_base[l] = ix->img_base[l];
@@ -187,6 +194,8 @@ static int run_kary(const Index* ix, const void* q, uint64_t m, void* out, cudaS
             p.flat = (const uint32_t*)ix->d_flat;
             p.flat64 = (const uint64_t*)ix->d_flat64;
             p.flat_D = ix->flat_D;
+            p.flat_M = ix->flat_M;
+            p.flat_span = ix->flat_span;
             p.smem_bytes = (4u << ix->flat_D) + 16;
         }
         ix->last_kary_smem = p.smem_bytes;

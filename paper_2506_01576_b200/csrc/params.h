@@ -57,6 +57,8 @@ struct KaryParams {
     const uint32_t* flat;    // staged from here (2^flat_D words; slot 0 unused)
     const uint64_t* flat64;  // exact u64 copy (tie redo), u64 keys only
     uint32_t flat_D;
+    uint64_t flat_M;         // node maxima in the table (sorted position c < flat_M)
+    uint64_t flat_span;      // keys under one flat-level node: max of node c = a[min((c+1)*span, n) - 1]
     // fused peer-memory routing (peer.cu, bs_lookup_peer; g1 kernels only).
     // peer_cursor == nullptr: a plain lookup.  Otherwise the kernel first waits
     // until *peer_wait >= peer_wait_target (every rank has routed its queries
