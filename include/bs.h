@@ -253,6 +253,15 @@ int bs_export(const void* idx, int what, void* dst, uint64_t cap, uint64_t* writ
  * but not ascending), BS_ERR_CUDA / BS_ERR_OOM. */
 int bs_merge(const void* idx, const void* delta_keys, uint64_t m, int delta_sorted, void** out_idx);
 
+/* Batch delete (same outlook): builds a NEW index, same layout, over
+ * idx's keys minus every key equal to one of the m device keys del_keys
+ * (set difference: all occurrences of a deleted value go; values not present
+ * are ignored; del_sorted = 1 if ascending, else the library sorts a copy).
+ * idx is untouched.  Synchronous.  m = 0 clones idx.  Errors: BS_ERR_INVALID
+ * (NULL, or every key erased: an index needs n >= 1), BS_ERR_UNSUPPORTED
+ * (multi-GPU index), BS_ERR_CUDA / BS_ERR_OOM. */
+int bs_erase(const void* idx, const void* del_keys, uint64_t m, int del_sorted, void** out_idx);
+
 /* Library version / build string (arch, commit-independent). */
 const char* bs_version(void);
 

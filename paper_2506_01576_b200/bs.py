@@ -103,10 +103,11 @@ def lib():
         L.bs_peer_status.argtypes = [vp, ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(_u64)]
         L.bs_peer_results.argtypes = [vp, ctypes.POINTER(vp)]
         L.bs_merge.argtypes = [vp, vp, _u64, i, ctypes.POINTER(vp)]
+        L.bs_erase.argtypes = [vp, vp, _u64, i, ctypes.POINTER(vp)]
         for f in ("bs_layout_default", "bs_launch_default", "bs_build", "bs_lookup", "bs_lookup_ex",
                   "bs_lookup_host", "bs_index_info", "bs_export", "bs_dist_get_uid", "bs_dist_init",
                   "bs_build_dist", "bs_lookup_dist", "bs_build_peer", "bs_peer_export", "bs_peer_connect",
-                  "bs_lookup_peer", "bs_peer_status", "bs_peer_results", "bs_merge"):
+                  "bs_lookup_peer", "bs_peer_status", "bs_peer_results", "bs_merge", "bs_erase"):
             getattr(L, f).restype = i
         _lib = L
     return _lib
@@ -220,6 +221,13 @@ def bs_merge(index: Index, delta_keys, m: int, delta_sorted: bool = False) -> In
     """New index over index's keys plus m delta keys (device), same layout."""
     h = ctypes.c_void_p()
     _check(lib().bs_merge(index.handle, _ptr(delta_keys), m, 1 if delta_sorted else 0, ctypes.byref(h)))
+    return Index(h.value, index.layout)
+
+
+def bs_erase(index: Index, del_keys, m: int, del_sorted: bool = False) -> Index:
+    """New index over index's keys minus every key equal to one of m device keys."""
+    h = ctypes.c_void_p()
+    _check(lib().bs_erase(index.handle, _ptr(del_keys), m, 1 if del_sorted else 0, ctypes.byref(h)))
     return Index(h.value, index.layout)
 
 

@@ -1,4 +1,4 @@
-"""Cost of batch inserts (P:254 outlook): bs_merge of a random
+"""Cost of batch inserts and deletes (P:254 outlook): bs_merge of a random
 delta into the config-3 index (2^26 u64 keys, K-ary layout) vs rebuilding
 from the unsorted concatenation (bs_build, library radix sort).  Host wall
 time of the synchronous calls, median of 3 after a warm-up.  One JSON line per
@@ -62,6 +62,19 @@ def main():
                           "speedup": t_rebuild / t_merge, "merged_array_exact": ok}), flush=True)
         del cat, dd
         torch.cuda.empty_cache()
+    # batch deletes: erase a random subset of the keys (plus as many absent values)
+    for frac in (0.001, 0.01, 0.1):
+        m = int(n * frac)
+        dele = np.concatenate([keys[rng.integers(0, n, size=m // 2)],
+                               rng.integers(0, np.iinfo(np.uint64).max, size=m - m // 2, dtype=np.uint64,
+                                            endpoint=True)])
+        dd = P.as_torch(dele)
+        t_erase = wall(lambda: bs.bs_erase(idx, dd, m))
+        new = bs.bs_erase(idx, dd, m)
+        got = bs.bs_export(new, bs.EXPORT_SORTED)
+        ok = bool(np.array_equal(got, keys[~np.isin(keys, dele)]))
+        new.close()
+        print(json.dumps({"n": n, "m_delete": m, "erase_ms": t_erase, "erased_array_exact": ok}), flush=True)
     idx.close()
 
 
