@@ -102,10 +102,11 @@ typedef struct {
                                    levels (node <= 64 B, 256-bit loads), C*key/32 lanes per
                                    lookup for the leaf (needs C*key in 32..256 B, else 2);
                                7 = 6 with the shared levels replaced by a binary search over
-                                   a pinned Eytzinger table of one level's node maxima;
-                               8 = BS_KARY_MODE_AUTO (layout default), resolved by bs_build:
-                                   7 when the sorted array is <= 2x the L2, else 6
-                                   (measured: profiles/r1s3t_modes_*, r1s3u_*)            */
+                                   a pinned Eytzinger table of one level's node maxima,
+                                   then that level's nodes in shared memory when they fit;
+                               8 = BS_KARY_MODE_AUTO (layout default), resolved by bs_build
+                                   to 7, the fastest at every measured size
+                                   (profiles/r1s3af_modes_*, r1s3ag_*)                    */
     uint32_t reserved[6];   /* must be 0                                                    */
 } bs_layout;
 

@@ -54,6 +54,7 @@ static void free_index(Index* ix) {
     if (ix->d_img64) cudaFree(ix->d_img64);
     if (ix->d_flat) cudaFree(ix->d_flat);
     if (ix->d_flat64) cudaFree(ix->d_flat64);
+    if (ix->d_flatimg) cudaFree(ix->d_flatimg);
     destroy_host_ctx(ix);
     destroy_dist_state(ix);
     destroy_peer_state(ix);
@@ -205,6 +206,22 @@ static int build_kary_layout(Index* ix, cudaStream_t st) {
         }
         e = build_flat_table(kb, ix->d_keys, n, span, ix->flat_M, D, ix->d_flat, ix->d_flat64, st);
         if (e != cudaSuccess) return fail_cuda(e, "build_flat_table");
+        // the flat level's node image next to the table (one buffer, one TMA
+        // stage): mode 7 then descends one shared level below the table
+        ix->flat_img_words = 0;
+        if (lt < L && lt < ix->img_L && ix->d_img) {
+            const uint64_t wl = ix->img_base[lt + 1] - ix->img_base[lt];   // 4-word multiple
+            if ((1ull << D) + wl <= cap_words) {
+                e = cudaMalloc(&ix->d_flatimg, ((1ull << D) + wl) * 4);
+                if (e != cudaSuccess) return fail_cuda(e, "cudaMalloc(flat table + level image)");
+                e = cudaMemcpyAsync(ix->d_flatimg, ix->d_flat, 4ull << D, cudaMemcpyDeviceToDevice, st);
+                if (e == cudaSuccess)
+                    e = cudaMemcpyAsync((uint32_t*)ix->d_flatimg + (1ull << D), (const uint32_t*)ix->d_img + ix->img_base[lt],
+                                        wl * 4, cudaMemcpyDeviceToDevice, st);
+                if (e != cudaSuccess) return fail_cuda(e, "flat table + level image");
+                ix->flat_img_words = (uint32_t)wl;
+            }
+        }
     }
     return BS_OK;
 }
@@ -296,11 +313,10 @@ int bs_build(const void* keys, uint64_t n, const bs_layout* layout_in, void** ou
     ix->hints_requested = ix->layout.cache_hints;
     ix->kary_mode_requested = ix->layout.kary_mode;
     if (ix->layout.kary_mode == BS_KARY_MODE_AUTO) {
-        // the pinned Eytzinger table (7) wins while the array stays near L2
-        // (u32 up to 2^25 keys: +10-18 %; u64 2^24: +30 %); at config 3 (512 MB)
-        // the per-level shared descent (6) is 3 % faster sustained
-        const uint64_t l2 = ix->l2_bytes ? (uint64_t)ix->l2_bytes : (126ull << 20);
-        ix->layout.kary_mode = (uint64_t)abytes <= 2 * l2 ? 7u : 6u;
+        // the pinned Eytzinger table + one shared node level (7) is the fastest
+        // thread-per-lookup schedule at every measured size (profiles/r1s3af_*,
+        // r1s3ag_*: config 3 +1.8 % sustained over 6, config 2 +22 %)
+        ix->layout.kary_mode = 7u;
     }
     if (ix->layout.cache_hints & BS_HINT_AUTO) {
         const uint64_t l2 = ix->l2_bytes ? (uint64_t)ix->l2_bytes : (126ull << 20);
@@ -490,6 +506,7 @@ int bs_index_info(const void* idx, bs_info* info) {
     if (ix->d_img) info->footprint_bytes += (uint64_t)ix->img_base[ix->img_L] * 4 * (ix->kb == 8 ? 2 : 1);
     if (ix->d_img64) info->footprint_bytes += (uint64_t)ix->img64_base[ix->img64_L] * 8;
     if (ix->d_flat) info->footprint_bytes += (1ull << ix->flat_D) * (ix->d_flat64 ? 12 : 4);
+    if (ix->d_flatimg) info->footprint_bytes += ((1ull << ix->flat_D) + ix->flat_img_words) * 4;
     info->build_ms = ix->build_ms;
     info->sm_count = ix->sm_count;
     info->smem_per_cta_opt = (uint32_t)ix->last_opt_smem;

@@ -79,6 +79,8 @@ struct Index {
     void* d_flat64 = nullptr;
     uint64_t flat_M = 0;             // node maxima stored (nodes - 1)
     uint64_t flat_span = 0;          // keys under one flat-level node
+    void* d_flatimg = nullptr;       // [flat table (2^flat_D words) | flat level's node image], one stage
+    uint32_t flat_img_words = 0;     // words of the level image (0: not built)
     uint32_t flat_level = 0, flat_D = 0;   // Eytzinger slots 1..2^flat_D - 1
 
     // device

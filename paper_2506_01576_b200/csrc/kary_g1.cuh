@@ -62,7 +62,7 @@ k_kary_g1(const KaryParams<K> p, const K* __restrict__ q, uint64_t m_arg, void* 
     const uint32_t gl = lane / GL;               // leaf group within the warp
     const uint32_t gm = GMASK << (gl * GL);
 
-    if (FLAT) stage_image<uint32_t, false>(S, p.flat, 0, 1u << p.flat_D, bar);
+    if (FLAT) stage_image<uint32_t, false>(S, p.flat, 0, (1u << p.flat_D) + p.flat_img_words, bar);
     else if (p.img_words) stage_image<uint32_t, false>(S, p.img, p.img_plane_words, p.img_words, bar);
 
     // fused peer routing (bs_lookup_peer): wait until every rank has routed
@@ -150,6 +150,17 @@ k_kary_g1(const KaryParams<K> p, const K* __restrict__ q, uint64_t m_arg, void* 
             }
 #pragma unroll
             for (int t = 0; t < T; ++t) node[t] = k[t] - (1u << D);
+            if (p.flat_img_words) {
+                // one more shared level: the flat level's node image follows the table
+                const uint32_t last = p.nodes_next[Ls - 1] - 1;
+#pragma unroll
+                for (int t = 0; t < T; ++t) {
+                    const uint32_t c = smem_node_rank<K, W, false, false>(S, (1u << D) + node[t] * (W + 1), key[t],
+                                                                          extra, tie);
+                    const uint32_t child = node[t] * K_ + c;
+                    node[t] = child < last ? child : last;
+                }
+            }
             if constexpr (sizeof(K) == 8) {
                 // hi-word ties: node = #(maxima whose hi word < q's), a lower
                 // bound on the exact count; the tied lanes step over the maxima

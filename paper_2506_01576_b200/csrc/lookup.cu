@@ -197,6 +197,22 @@ static int run_kary(const Index* ix, const void* q, uint64_t m, void* out, cudaS
             p.flat_M = ix->flat_M;
             p.flat_span = ix->flat_span;
             p.smem_bytes = (4u << ix->flat_D) + 16;
+            p.flat_img_words = 0;
+            const uint64_t with_img = ((1ull << ix->flat_D) + ix->flat_img_words) * 4 + 16;
+            // (not for the pipelined FLAT kernel, T = 3, which stages the table alone)
+            const bool pipelined = (L.nreg >> 4) >= 3 && !pl;
+            if (ix->d_flatimg && !pipelined && with_img <= smem_cap(ix, L.ctas_per_sm ? L.ctas_per_sm : 1)) {
+                // table + the flat level's node image: one shared level more
+                const uint32_t fl = ix->flat_level;
+                p.Ls = fl + 1;
+                p.flat = (const uint32_t*)ix->d_flatimg;
+                p.flat_img_words = ix->flat_img_words;
+                p.smem_bytes = (uint32_t)with_img;
+                uint64_t span = ix->kC;
+                for (uint32_t l = fl + 1; l < ix->kL; ++l) span *= ix->kK;
+                p.flat_span = span;                 // tie fix-up at level fl + 1
+                p.flat_M = ix->k_next[fl] - 1;
+            }
         }
         ix->last_kary_smem = p.smem_bytes;
         // nreg: low 4 bits = leaf waves in flight IL (default 4), bits 4.. = lookups

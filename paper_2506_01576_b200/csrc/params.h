@@ -58,7 +58,8 @@ struct KaryParams {
     const uint64_t* flat64;  // exact u64 copy (tie redo), u64 keys only
     uint32_t flat_D;
     uint64_t flat_M;         // node maxima in the table (sorted position c < flat_M)
-    uint64_t flat_span;      // keys under one flat-level node: max of node c = a[min((c+1)*span, n) - 1]
+    uint64_t flat_span;      // keys under one node of level Ls: max of node c = a[min((c+1)*span, n) - 1]
+    uint32_t flat_img_words; // > 0: the flat level's node image follows the table in smem (mode 7 descends it)
     // fused peer-memory routing (peer.cu, bs_lookup_peer; g1 kernels only).
     // peer_cursor == nullptr: a plain lookup.  Otherwise the kernel first waits
     // until *peer_wait >= peer_wait_target (every rank has routed its queries
