@@ -166,10 +166,12 @@ typedef struct {
 #define BS_EXPORT_PINNED 1   /* the level-major pinned table (pinned_entries keys)     */
 #define BS_EXPORT_KARY 2     /* K-ary separator slots, levels top-first (separator_slots) */
 
-/* Fills *l with defaults for u64 keys/outputs, K-ary K = 5 / C = 16 with the
- * thread-per-lookup schedule (kary_mode 6; the fastest measured on B200 for
- * 2^26 u64 keys, DESIGN.md §6.1 — the paper's A6000 optimum was K = 17,
- * P:223), largest pin budget, static schedule.  BS_ERR_INVALID if l is NULL. */
+/* Fills *l with defaults for u64 keys/outputs: K-ary, K = 5 (the paper's
+ * A6000 optimum was K = 17), leaf chunk, schedule and
+ * L2 hints left to bs_build (leaf_chunk = 0, kary_mode = BS_KARY_MODE_AUTO,
+ * cache_hints = BS_HINT_AUTO: at 2^26 u64 keys they resolve to C = 16, the
+ * thread-per-lookup kary_mode 7 and stream + separator hints), largest pin
+ * budget, static schedule.  BS_ERR_INVALID if l is NULL. */
 int bs_layout_default(bs_layout* l);
 
 /* Fills *l with the per-call defaults stored in idx. */

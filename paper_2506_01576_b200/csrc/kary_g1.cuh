@@ -1,5 +1,5 @@
 // kary_g1.cuh — K-ary search (§5), "thread-per-lookup"
-// B200 schedule for small nodes (kary_mode 6).
+// B200 schedule for small nodes (kary_mode 6, and 7 = the bench default).
 //
 // Same index and result as kary.cu.  Designed around the two limits the
 // tiered schedule (kary_tiered.cuh) runs into on B200 — issue slots and L1
