@@ -219,8 +219,10 @@ k_kary_g1(const KaryParams<K> p, const K* __restrict__ q, uint64_t m_arg, void* 
             const K* lv = p.sep + p.lvl_base[l];
             const uint32_t last = p.nodes_next[l] - 1;
             K s[T][W];
+            // evict_last only for the levels that fit L2 (cumulative); deeper ones stream like leaves
+            const uint64_t pol_l = l < p.sep_last_end ? pol_sep : pol_leaf;
 #pragma unroll
-            for (int t = 0; t < T; ++t) ld_node<K, W>(lv + (uint64_t)node[t] * W, true, pol_sep, s[t]);
+            for (int t = 0; t < T; ++t) ld_node<K, W>(lv + (uint64_t)node[t] * W, true, pol_l, s[t]);
 #pragma unroll
             for (int t = 0; t < T; ++t) {
                 uint32_t c = 0;

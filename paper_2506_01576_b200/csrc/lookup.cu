@@ -159,6 +159,18 @@ static int run_kary(const Index* ix, const void* q, uint64_t m, void* out, cudaS
     p.stream_hint = (L.cache_hints & BS_HINT_STREAM_EVICT_FIRST) ? 1 : 0;
     p.leaf_hint = (L.cache_hints & BS_HINT_LEAF_EVICT_FIRST) ? 1 : 0;
     p.sep_hint = (L.cache_hints & BS_HINT_SEP_EVICT_LAST) ? 1 : 0;
+    {   // separator levels (top-first) whose cumulative bytes fit half the L2 keep evict_last
+        const uint64_t l2 = ix->l2_bytes ? (uint64_t)ix->l2_bytes : (126ull << 20);
+        uint64_t cum = 0;
+        uint32_t end = 0;
+        while (end < ix->kL) {
+            const uint64_t lb = ix->k_nodes[end] * ix->kW * ix->kb;
+            if (cum + lb > l2 / 2) break;
+            cum += lb;
+            ++end;
+        }
+        p.sep_last_end = end;
+    }
     const uint32_t smem = sbytes + 16;
     ix->last_kary_smem = smem;
     bool uns = false;

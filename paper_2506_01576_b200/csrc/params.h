@@ -48,6 +48,7 @@ struct KaryParams {
     uint32_t stream_hint;
     uint32_t leaf_hint;
     uint32_t sep_hint;       // 1: global separator levels with L2 evict_last
+    uint32_t sep_last_end;   // levels >= this get the leaf policy instead (deep levels > L2/2 cumulative)
     // tiered schedule: shared-memory image (Index::d_img), levels 0..Ls-1
     const uint32_t* img;     // hi plane (u64) / the plane (u32), then the lo plane
     uint64_t img_plane_words;// words per plane in global memory
