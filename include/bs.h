@@ -338,9 +338,11 @@ void bs_dist_destroy(void* comm);
 
 /* Builds this rank's index over its local ascending keys (device pointer,
  * n_local >= 1; layout must give variant KARY and out_bytes 8) and allocates
- * its IPC-exportable window: receive slots (recv_capacity keys + 8-B tags;
- * 0 = world * max_m_local, which can never overflow) and a return window of
- * max_m_local results.  max_m_local < 2^32 bounds m_local of later lookups.
+ * its IPC-exportable window: receive slots (recv_capacity keys + 4-B return
+ * tags, (src_rank << (32 - ceil(log2 world))) | src_idx; recv_capacity 0 =
+ * world * max_m_local, which can never overflow) and a return window of
+ * max_m_local results.  max_m_local bounds m_local of later lookups and must
+ * be < 2^32 and <= 2^(32 - ceil(log2 world)) (2^29 at world 8).
  * Not collective.  Errors: BS_ERR_INVALID (bad rank/world/sizes/layout),
  * BS_ERR_UNSUPPORTED (variant is not KARY), BS_ERR_OOM, plus bs_build's. */
 int bs_build_peer(const void* local_keys, uint64_t n_local, const bs_layout* layout, int rank, int world,

@@ -20,13 +20,14 @@ struct PeerLaunch {
     unsigned long long* cursor;
     const unsigned long long* wait;
     unsigned long long target;
-    const uint64_t* tag;
+    const uint32_t* tag;
     uint64_t* const* ret;
     unsigned long long* const* sig;
     unsigned* done;
     unsigned* err;
     uint64_t base;
     uint32_t P;
+    uint32_t shift;   // tag = (src_rank << shift) | src_idx
 };
 
 struct Index {

@@ -112,12 +112,12 @@ k_kary_g1(const KaryParams<K> p, const K* __restrict__ q, uint64_t m_arg, void* 
         }
         // PEER: each owner lane fetches its slot's return tag now; the load is
         // hidden behind the descent, the leaf epilogue takes it by shuffle
-        uint64_t tag_own[T];
+        uint32_t tag_own[T];
         if constexpr (PEER) {
 #pragma unroll
             for (int t = 0; t < T; ++t) {
                 const uint64_t i = (wt + t) * 32 + lane;
-                tag_own[t] = i < m ? __ldcg(p.peer_tag + i) : 0ull;
+                tag_own[t] = i < m ? __ldcg(p.peer_tag + i) : 0u;
             }
         }
         // ---- shared-memory levels: hi words only, exact redo on a tie ----
@@ -261,7 +261,7 @@ k_kary_g1(const KaryParams<K> p, const K* __restrict__ q, uint64_t m_arg, void* 
                 const bool last_lt = x[i][VL - 1] < kk[i];
                 lt = group_sum<GL>(lt, gl, fb_leaf);
                 const bool any_eq = (__ballot_sync(0xFFFFFFFFu, eq) & gm) != 0;
-                uint64_t tg = 0;
+                uint32_t tg = 0;
                 if constexpr (PEER) tg = __shfl_sync(0xFFFFFFFFu, tag_own[t], (b * IL + i) * GPWL + (int)gl);
                 if (jl == GL - 1) {
                     const uint64_t lbv = (uint64_t)cc[i] * C + lt + (last_lt ? 1u : 0u);
@@ -273,7 +273,9 @@ k_kary_g1(const KaryParams<K> p, const K* __restrict__ q, uint64_t m_arg, void* 
                         if constexpr (PEER) {
                             // result straight into the source rank's return window (P2P store)
                             const uint64_t g = lbv + p.peer_base;
-                            p.peer_ret[tg >> 32][tg & 0xFFFFFFFFull] = hit ? g : (g | miss);
+                            // 4-B tag: rank in the top bits (u64 shift: peer_shift = 32 at P = 1)
+                            const uint32_t sh = p.peer_shift;
+                            p.peer_ret[(uint64_t)tg >> sh][tg & (uint32_t)((1ull << sh) - 1ull)] = hit ? g : (g | miss);
                         } else if (ob == 8) {
                             store_stream((uint64_t*)out + o, res, true, pol_stream);
                         } else {

@@ -142,6 +142,7 @@ static int run_kary(const Index* ix, const void* q, uint64_t m, void* out, cudaS
         p.peer_err = pl->err;
         p.peer_base = pl->base;
         p.peer_P = pl->P;
+        p.peer_shift = pl->shift;
     }
     const bool tiered = !g1 && L.kary_mode >= 2 && C >= W && (C / W == 1 || C / W == 2 || C / W == 4);
     const bool pair64 = (L.kary_mode == 3 || L.kary_mode == 5) && ix->kb == 8;

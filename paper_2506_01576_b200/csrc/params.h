@@ -67,18 +67,20 @@ struct KaryParams {
     // into this rank's receive window), looks up min(m, *peer_cursor) slots,
     // and stores each result (global rank = peer_base + local lb, miss bit
     // kept) straight into the source rank's return window, slot
-    // peer_tag[o] = (src_rank << 32) | src_idx.  The last CTA to finish zeroes
+    // peer_tag[o] = (src_rank << peer_shift) | src_idx (4 B; peer_shift = 32 -
+    // ceil(log2 P), so src_idx < 2^peer_shift).  The last CTA to finish zeroes
     // the cursor and bumps every rank's return counter (*peer_sig[r]).
     unsigned long long* peer_cursor;
     const unsigned long long* peer_wait;
     unsigned long long peer_wait_target;
-    const uint64_t* peer_tag;
+    const uint32_t* peer_tag;
     uint64_t* const* peer_ret;             // [P] return windows (peer pointers)
     unsigned long long* const* peer_sig;   // [P] return-done counters (peer pointers)
     unsigned int* peer_done;               // local CTA completion counter
     unsigned int* peer_err;                // local error bits (peer_sync.cuh)
     uint64_t peer_base;
     uint32_t peer_P;
+    uint32_t peer_shift;
 };
 
 // ---- launchers (return cudaGetLastError() after the launch) ----

@@ -8,7 +8,7 @@
 //   k_peer_route   shard = first s with shard_max[s] >= q (else P-1); per
 //                  4096-query tile, one system-scope atomicAdd per shard on
 //                  rank s's receive cursor claims a slot range; the query and
-//                  its tag (me << 32 | i) are stored straight into rank s's
+//                  its 4-B tag (me << shift | i) are stored straight into rank s's
 //                  receive window.  The last CTA bumps every rank's route
 //                  counter.
 //   k_kary_g1      (kary_g1.cuh, peer prologue/epilogue) waits for its route
@@ -37,7 +37,7 @@ namespace bs {
 
 constexpr int kPeerMaxRanks = 64;
 constexpr uint32_t kPeerMagic = 0x52505342u;   // "BSPR"
-constexpr uint32_t kPeerVersion = 1;
+constexpr uint32_t kPeerVersion = 2;   // 2: 4-byte return tags
 
 // what every rank sees of rank r (pointers valid in THIS process)
 struct PeerDev {
@@ -45,7 +45,7 @@ struct PeerDev {
     unsigned long long* ret_sig;     // rank r's return counter
     unsigned long long* cursor;      // rank r's receive cursor
     void* win_q;                     // rank r's receive window: keys
-    uint64_t* win_tag;               // rank r's receive window: (src_rank << 32) | src_idx
+    uint32_t* win_tag;               // rank r's receive window: (src_rank << shift) | src_idx
     uint64_t* ret;                   // rank r's return window (max_m results)
 };
 
@@ -69,13 +69,21 @@ struct RegionLayout {
     uint64_t q, tag, ret, total;
 };
 
+// 4-byte return tags: the source rank in the top ceil(log2 P) bits, the
+// source index below (so every rank's max_m_local must be <= 2^shift)
+static uint32_t tag_shift(uint32_t P) {
+    uint32_t b = 0;
+    while ((1u << b) < P) ++b;
+    return 32 - b;
+}
+
 static uint64_t align256(uint64_t x) { return (x + 255) & ~255ull; }
 
 static RegionLayout region_layout(uint64_t cap, uint64_t max_m, uint32_t kb) {
     RegionLayout L;
     L.q = 256;
     L.tag = align256(L.q + cap * kb);
-    L.ret = align256(L.tag + cap * 8);
+    L.ret = align256(L.tag + cap * 4);
     L.total = align256(L.ret + (max_m ? max_m : 1) * 8);
     return L;
 }
@@ -123,7 +131,8 @@ template <class K>
 __global__ void __launch_bounds__(kRouteThreads) k_peer_route(const K* __restrict__ q, uint64_t m,
                                                               const PeerDev* __restrict__ peers,
                                                               const uint64_t* __restrict__ shard_max, uint32_t P,
-                                                              uint32_t me, uint64_t cap, unsigned* done, unsigned* err) {
+                                                              uint32_t me, uint32_t shift, uint64_t cap, unsigned* done,
+                                                              unsigned* err) {
     __shared__ K s_max[kPeerMaxRanks];
     __shared__ PeerDev s_peer[kPeerMaxRanks];
     __shared__ unsigned s_cnt[kPeerMaxRanks];
@@ -171,7 +180,7 @@ __global__ void __launch_bounds__(kRouteThreads) k_peer_route(const K* __restric
             const uint64_t slot = s_base[dst[j]] + rnk[j];
             if (slot < cap) {
                 ((K*)s_peer[dst[j]].win_q)[slot] = key[j];
-                s_peer[dst[j]].win_tag[slot] = ((uint64_t)me << 32) | (i0 + (uint64_t)j * kRouteThreads);
+                s_peer[dst[j]].win_tag[slot] = (uint32_t)(((uint64_t)me << shift) | (i0 + (uint64_t)j * kRouteThreads));
             } else {
                 atomicOr(err, kPeerErrOverflow);
             }
@@ -209,7 +218,8 @@ int bs_build_peer(const void* local_keys, uint64_t n_local, const bs_layout* lay
     *out_idx = nullptr;
     if (world < 1 || world > kPeerMaxRanks || rank < 0 || rank >= world)
         return fail(BS_ERR_INVALID, "bs_build_peer: need 0 <= rank < world <= %d", kPeerMaxRanks);
-    if (max_m_local >= (1ull << 32)) return fail(BS_ERR_INVALID, "bs_build_peer: max_m_local must be < 2^32");
+    if (max_m_local >= (1ull << 32) || max_m_local > (1ull << tag_shift((uint32_t)world)))
+        return fail(BS_ERR_INVALID, "bs_build_peer: max_m_local must be < 2^32 and <= 2^(32 - ceil(log2 world)) (4-B tags)");
     int rc = bs_build(local_keys, n_local, layout, out_idx);
     if (rc != BS_OK) return rc;
     Index* ix = (Index*)*out_idx;
@@ -327,7 +337,7 @@ int bs_peer_connect(void* idx, const void* blobs) {
         }
         const RegionLayout L = region_layout(B[r].cap, B[r].max_m, ix->kb);
         PeerCtl* c = (PeerCtl*)base;
-        pd[r] = PeerDev{&c->route_sig, &c->ret_sig, &c->cursor, base + L.q, (uint64_t*)(base + L.tag),
+        pd[r] = PeerDev{&c->route_sig, &c->ret_sig, &c->cursor, base + L.q, (uint32_t*)(base + L.tag),
                         (uint64_t*)(base + L.ret)};
         rp[r] = pd[r].ret;
         sp[r] = pd[r].ret_sig;
@@ -358,16 +368,16 @@ int bs_lookup_peer(const void* idx, const void* local_queries, uint64_t m_local,
     const unsigned gr = (unsigned)(tiles < 1 ? 1 : tiles > (uint64_t)ix->sm_count * 8 ? (uint64_t)ix->sm_count * 8 : tiles);
     if (ix->kb == 8)
         k_peer_route<uint64_t><<<gr, 256, 0, s>>>((const uint64_t*)local_queries, m_local, d->d_peers, d->d_shard_max, P,
-                                                  me, d->cap, &c->done_route, &c->err);
+                                                  me, tag_shift(P), d->cap, &c->done_route, &c->err);
     else
         k_peer_route<uint32_t><<<gr, 256, 0, s>>>((const uint32_t*)local_queries, m_local, d->d_peers, d->d_shard_max, P,
-                                                  me, d->cap, &c->done_route, &c->err);
+                                                  me, tag_shift(P), d->cap, &c->done_route, &c->err);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail_cuda(e, "k_peer_route launch");
     bs_launch L;
     bs_launch_default(idx, &L);
-    PeerLaunch pl{&c->cursor, &c->route_sig, target, (const uint64_t*)(d->region + d->lay.tag), d->d_ret, d->d_sig,
-                  &c->done_look, &c->err, d->base[me], P};
+    PeerLaunch pl{&c->cursor, &c->route_sig, target, (const uint32_t*)(d->region + d->lay.tag), d->d_ret, d->d_sig,
+                  &c->done_look, &c->err, d->base[me], P, tag_shift(P)};
     // once the route kernel is queued the call is committed: every rank waits
     // for this one, so a failure past this point is fatal for the group
     d->epoch += 1;

@@ -61,6 +61,16 @@ def test_peer_overflow_flagged():
     idx.close()
 
 
+def test_peer_max_m_bound_for_4byte_tags():
+    """Return tags are 4 B: (src_rank << (32 - ceil(log2 world))) | src_idx, so
+    max_m_local above 2^(32 - ceil(log2 world)) is rejected before any allocation."""
+    keys = workload.gen_keys(1000, 8, seed=5)
+    for world, limit in ((8, 1 << 29), (3, 1 << 30), (2, 1 << 31), (1, (1 << 32) - 1)):
+        with pytest.raises(bs.BsError) as e:
+            bs.bs_build_peer(P.as_torch(keys), keys.size, _layout(8), 0, world, limit + 1, recv_capacity=16)
+        assert e.value.code == bs.BS_ERR_INVALID
+
+
 def test_peer_connect_checks_order():
     a = workload.gen_keys(1000, 8, seed=5)
     lo, hi = a[:500], a[500:]
