@@ -191,13 +191,34 @@ __global__ void __launch_bounds__(kRouteThreads) k_peer_route(const K* __restric
         for (uint32_t r = 0; r < P; ++r) red_release_sys_add_u64(s_peer[r].route_sig, 1ull);
 }
 
+constexpr int kFinishUnroll = 4;
+
 __global__ void __launch_bounds__(256) k_peer_finish(const uint64_t* ret, uint64_t m, uint64_t* __restrict__ out,
                                                      const unsigned long long* ret_sig, unsigned long long target,
                                                      unsigned* err) {
     if (threadIdx.x == 0) peer_wait_ge(ret_sig, target, err);
     __syncthreads();
+    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) out[i] = __ldcg(ret + i);
+    if (((uintptr_t)out & 15) == 0) {
+        // 16-B accesses, kFinishUnroll independent loads in flight per thread: a
+        // plain 8-B grid-stride copy is latency-bound (too few bytes in flight)
+        const ulonglong2* r2 = (const ulonglong2*)ret;   // the window is 256-B aligned
+        ulonglong2* o2 = (ulonglong2*)out;
+        const uint64_t m2 = m >> 1;
+        uint64_t i = tid;
+        for (; i + (kFinishUnroll - 1) * stride < m2; i += kFinishUnroll * stride) {
+            ulonglong2 v[kFinishUnroll];
+#pragma unroll
+            for (int u = 0; u < kFinishUnroll; ++u) v[u] = __ldcg(r2 + i + u * stride);
+#pragma unroll
+            for (int u = 0; u < kFinishUnroll; ++u) __stcs(o2 + i + u * stride, v[u]);
+        }
+        for (; i < m2; i += stride) __stcs(o2 + i, __ldcg(r2 + i));
+        if (tid == 0 && (m & 1)) out[m - 1] = __ldcg(ret + m - 1);
+    } else {
+        for (uint64_t i = tid; i < m; i += stride) out[i] = __ldcg(ret + i);
+    }
 }
 
 static unsigned grid_for(uint64_t work, unsigned cap_ctas) {
@@ -385,7 +406,7 @@ int bs_lookup_peer(const void* idx, const void* local_queries, uint64_t m_local,
     if (rc != BS_OK) return rc;
     // out_local == NULL: the results stay in the return window (bs_peer_results)
     const uint64_t mc = out_local ? m_local : 0;
-    k_peer_finish<<<grid_for(mc, (unsigned)ix->sm_count * 4), 256, 0, s>>>(
+    k_peer_finish<<<grid_for(mc / 2, (unsigned)ix->sm_count * 8), 256, 0, s>>>(
         (const uint64_t*)(d->region + d->lay.ret), mc, (uint64_t*)out_local, &c->ret_sig, target, &c->err);
     e = cudaGetLastError();
     if (e != cudaSuccess) return fail_cuda(e, "k_peer_finish launch");

@@ -43,8 +43,13 @@ def test_peer_world1(kb):
             got = P.to_numpy_unsigned(out[:m], 8)
             want = oracle.lookup(keys, q, out_bytes=8)
             assert np.array_equal(got, want), f"call {call}: first mismatch at {np.flatnonzero(got != want)[:5]}"
+    # out only 8-B aligned: the finish kernel's scalar copy
+    q = workload.gen_queries(keys, 4097, seed=7, hit_ratio=0.5)
+    bs.bs_lookup_peer(idx, P.as_torch(q), q.size, out[1:])
+    torch.cuda.synchronize()
+    assert np.array_equal(P.to_numpy_unsigned(out[1:1 + q.size], 8), oracle.lookup(keys, q, out_bytes=8))
     err, calls = bs.bs_peer_status(idx)
-    assert err == 0 and calls == 5
+    assert err == 0 and calls == 6
     idx.close()
 
 
