@@ -45,9 +45,12 @@ __device__ __forceinline__ void ld_node(const K* p, bool hint, uint64_t pol, K* 
     }
 }
 
-template <class K, int W, int GL, int IL, int T, bool FLAT, bool PEER = false>
+// OBC != 0: the output width is a compile-time constant (the FLAT T = 1
+// instance for out_bytes == key_bytes), so the epilogue carries no width select
+template <class K, int W, int GL, int IL, int T, bool FLAT, bool PEER = false, int OBC = 0>
 __global__ void __launch_bounds__(T >= 2 ? 768 : 1024, 1)
-k_kary_g1(const KaryParams<K> p, const K* __restrict__ q, uint64_t m_arg, void* __restrict__ out, uint32_t ob) {
+k_kary_g1(const KaryParams<K> p, const K* __restrict__ q, uint64_t m_arg, void* __restrict__ out, uint32_t ob_arg) {
+    const uint32_t ob = OBC ? (uint32_t)OBC : ob_arg;
     constexpr int VL = 32 / (int)sizeof(K);     // leaf keys per lane (one 256-bit load)
     constexpr int GPWL = 32 / GL;               // leaf lookups per wave
     constexpr uint32_t GMASK = (GL == 32) ? 0xFFFFFFFFu : ((1u << GL) - 1u);
@@ -442,6 +445,10 @@ static cudaError_t go_g1(const void* params, const void* q, uint64_t m, void* ou
     auto kern = flat ? (T >= 2 ? k_kary_g1<K, W, GL, IL, 2, true> : k_kary_g1<K, W, GL, IL, 1, true>)
                      : (T >= 2 ? k_kary_g1<K, W, GL, IL, 2, false> : k_kary_g1<K, W, GL, IL, 1, false>);
     if (peer) kern = flat ? k_kary_g1<K, W, GL, IL, 1, true, true> : k_kary_g1<K, W, GL, IL, 1, false, true>;
+    // BS_G1_RUNTIME_OB=1 keeps the runtime-width instance (A/B knob, not part of the ABI)
+    static const bool runtime_ob = getenv("BS_G1_RUNTIME_OB") != nullptr;
+    if (flat && T == 1 && !peer && ob == sizeof(K) && !runtime_ob)
+        kern = k_kary_g1<K, W, GL, IL, 1, true, false, (int)sizeof(K)>;
     if (flat && T == 3 && !peer) kern = k_kary_g1p<K, W, GL, IL>;   // T = 3 encodes "pipelined, one lookup per thread"
     cudaFuncAttributes fa;
     cudaError_t e = cudaFuncGetAttributes(&fa, kern);
