@@ -131,28 +131,38 @@ k_kary_g1(const KaryParams<K> p, const K* __restrict__ q, uint64_t m_arg, void* 
         if constexpr (FLAT) {
             // binary search over the pinned Eytzinger table of level-Ls node maxima:
             // k <- 2k + [T[k] < q] for D levels; the rank k - 2^D is the node
+            // The recurrence runs on the shared ADDRESS a = sb + 4k: a' = 2a - sb +
+            // 4[T[k] < q] is one SEL + one IMAD per level (no index -> address step).
+            // u64 hi-word ties: a table entry on the path equals q's hi word iff the
+            // last left-turn node (k >> ffs(~k), the lower-bound entry) does — every
+            // left turn below a tied node stays within [qh, qh] — so one probe after
+            // the loop replaces a compare per level.
             const uint32_t D = p.flat_D;
-            uint32_t k[T];
+            const uint32_t sb = smem_u32(S);
+            const uint32_t step_lt = 4u - sb, step_ge = 0u - sb;
+            uint32_t a[T], k[T];
 #pragma unroll
-            for (int t = 0; t < T; ++t) k[t] = 1;
+            for (int t = 0; t < T; ++t) a[t] = sb + 4u;
 #pragma unroll 4
             for (uint32_t d = 0; d < D; ++d) {
 #pragma unroll
                 for (int t = 0; t < T; ++t) {
-                    const uint32_t h = S[k[t]];
+                    const uint32_t h = lds_u32(a[t]);
                     bool less;
-                    if constexpr (sizeof(K) == 8) {
-                        const uint32_t qh = (uint32_t)((uint64_t)key[t] >> 32);
-                        less = h < qh;
-                        tie |= h == qh;
-                    } else {
-                        less = h < (uint32_t)key[t];
-                    }
-                    k[t] = 2 * k[t] + (less ? 1u : 0u);
+                    if constexpr (sizeof(K) == 8) less = h < (uint32_t)((uint64_t)key[t] >> 32);
+                    else less = h < (uint32_t)key[t];
+                    a[t] = 2u * a[t] + (less ? step_lt : step_ge);
                 }
             }
 #pragma unroll
-            for (int t = 0; t < T; ++t) node[t] = k[t] - (1u << D);
+            for (int t = 0; t < T; ++t) {
+                k[t] = (a[t] - sb) >> 2;
+                node[t] = k[t] - (1u << D);
+                if constexpr (sizeof(K) == 8) {
+                    const uint32_t j = k[t] >> __ffs(~k[t]);
+                    tie |= j != 0 && S[j] == (uint32_t)((uint64_t)key[t] >> 32);
+                }
+            }
             if (p.flat_img_words) {
                 // one more shared level: the flat level's node image follows the table
                 const uint32_t last = p.nodes_next[Ls - 1] - 1;

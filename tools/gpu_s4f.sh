@@ -3,7 +3,7 @@
 set -u
 mkdir -p gpurun_out
 T=${TAG:-r1s4f}
-timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fullsize.py tests/test_gpu_peer.py -q -rf -x --timeout 900 > gpurun_out/${T}_pytest.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/${T}_pytest.log
+timeout 1200 python -m pytest tests -m gpu -q -rf -x --timeout 900 > gpurun_out/${T}_pytest.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/${T}_pytest.log
 for r in 1 2 3; do
   for ab in runtime const; do
     if [ $ab = runtime ]; then export BS_G1_RUNTIME_OB=1; else unset BS_G1_RUNTIME_OB; fi
