@@ -73,3 +73,61 @@ def test_golden_checksums(golden_dir):
         q = workload.gen_queries(keys, case["m"], seed=case["query_seed"], hit_ratio=case["hit_ratio"])
         assert hashlib.sha256(keys.tobytes()).hexdigest() == case["keys_sha256"]
         assert hashlib.sha256(q.tobytes()).hexdigest() == case["queries_sha256"]
+
+
+# ---- workload/device.py: the same generator in torch int64 ops (CPU here, CUDA in test_gpu_workload.py)
+
+def _bits(t):
+    import torch
+    return t.numpy().view(np.uint64 if t.dtype == torch.int64 else np.uint32)
+
+
+@pytest.mark.parametrize("kb,n,seed", [(4, 1, 3), (4, 1000, 42), (4, 1 << 20, 7), (8, 1 << 16, 42),
+                                       (8, 12345, 9), (4, 3 << 20, 11)])
+def test_device_generator_keys_match_numpy(kb, n, seed):
+    from workload import device as wd
+    want = workload.gen_keys(n, kb, seed=seed)
+    got = _bits(wd.gen_keys(n, kb, seed=seed, device="cpu"))
+    assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("kb,n,m,hr,order,start", [
+    (8, 1 << 12, 50000, 1.0, "random", 0), (8, 12345, 40000, 0.5, "random", 777),
+    (4, 1000, 65536, 0.5, "random", 0), (4, 1 << 14, 30000, 1.0, "sorted", 5),
+    (8, 3000, 20000, 0.0, "sorted", 0), (4, 7, 5000, 0.25, "random", 1 << 40)])
+def test_device_generator_queries_match_numpy(kb, n, m, hr, order, start):
+    import torch
+    from workload import device as wd
+    keys = workload.gen_keys(n, kb, seed=21)
+    want = workload.gen_queries(keys, m, seed=22, hit_ratio=hr, order=order, start=start)
+    tk = torch.from_numpy(keys.view(np.int64 if kb == 8 else np.int32))
+    got = _bits(wd.gen_queries(tk, m, seed=22, hit_ratio=hr, order=order, start=start, chunk=1 << 13))
+    assert np.array_equal(got, want)
+
+
+def test_device_generator_unsigned_helpers():
+    import torch
+    from workload import device as wd
+    x = np.array([0, 1, (1 << 63) - 1, 1 << 63, (1 << 64) - 1, 0x8000000000000001, 12345678901234567890],
+                 dtype=np.uint64)
+    t = torch.from_numpy(x.view(np.int64))
+    assert np.array_equal(_bits(wd.sort_unsigned(t)), np.sort(x))
+    for k in (1, 17, 31, 32, 63):
+        assert np.array_equal(_bits(wd._lsr(t, k)), x >> np.uint64(k))
+    for nn in (3, 1000, (1 << 33) + 7, 5):
+        assert np.array_equal(wd._umod(t, nn).numpy().astype(np.uint64), x % np.uint64(nn))
+    assert np.array_equal(_bits(wd.splitmix64(t)), workload.splitmix64(x))
+
+
+def test_device_generator_range_keys():
+    """Config-5 shard keys: unique, ascending, inside [lo, hi), roughly uniform."""
+    from workload import device as wd
+    N = 8
+    for s in (0, 3, 7):
+        lo, hi = s << 61, (s + 1) << 61
+        k = _bits(wd.gen_keys_range(1 << 16, lo, hi, seed=5, shard=s, device="cpu"))
+        assert k.size == 1 << 16 and np.all(k[1:] > k[:-1])
+        assert int(k[0]) >= lo and int(k[-1]) < hi
+        h = np.bincount(((k - np.uint64(lo)) >> np.uint64(61 - 4)).astype(np.int64), minlength=16)
+        assert h.min() > 0.8 * h.mean() and h.max() < 1.2 * h.mean()
+    assert N == 8
