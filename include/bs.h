@@ -58,8 +58,14 @@ typedef enum {
 typedef enum {
     BS_REORDER_NONE = 0,
     BS_REORDER_LOOKUP = 1, /* §4.3 "lookup-reordering": block-local sort, direct stores */
-    BS_REORDER_FULL = 2    /* §4.3 "full-reordering": + inverse permutation before a coalesced
+    BS_REORDER_FULL = 2,   /* §4.3 "full-reordering": + inverse permutation before a coalesced
                               store (Listing 2 l.35-39)                                 */
+    BS_REORDER_SORTED = 3  /* the batch is ordered (Fig. 1b): segment-staged lookup —
+                              per segment of 8192 keys one CTA stages a 32-bit order-preserving
+                              image in shared memory and searches its share of the (sorted)
+                              batch there.  Any variant's index.  Correct for ANY batch order
+                              (queries outside their segment's range take a global
+                              bisection); fast only when the batch is ascending.             */
 } bs_reorder;
 
 /* Build-time structure + default launch configuration.
@@ -80,7 +86,7 @@ typedef struct {
                                kept in shared memory (§5.1); 0 = no pinning;
                                0xFFFFFFFF = largest that fits                              */
     uint32_t pin_partial;   /* OPT: 1 = "full-pinning" (partial step M+1), 0 = "steps-pinning" */
-    uint32_t reorder;       /* bs_reorder (OPT only)                                        */
+    uint32_t reorder;       /* bs_reorder: 1-2 OPT only; 3 (SORTED) any variant             */
     uint32_t k;             /* KARY fan-out K, 2..33 (P:223 A6000 best K = 17)       */
     uint32_t leaf_chunk;    /* KARY leaf chunk C in keys, power of two 1..256; 0 =
                                auto (layout default), resolved by bs_build: the smallest
@@ -203,8 +209,14 @@ int bs_build(const void* keys, uint64_t n, const bs_layout* layout, void** out_i
  *   out      device pointer, m words of out_bytes; must not overlap queries.
  *   stream   cudaStream_t (void*); the call is stream-ordered and
  *            asynchronous: no allocation, no host synchronisation.
- * Errors: BS_ERR_INVALID (NULL idx / pointers with m > 0, overlap),
+ * Errors: BS_ERR_INVALID (NULL idx / pointers with m > 0, overlap, misaligned,
+ * or queries / out not device memory of the index's GPU — checked with
+ * cudaPointerGetAttributes; host buffers go through bs_lookup_host),
  * BS_ERR_CUDA (launch failure).
+ * Kernel attributes, the dynamic shared memory limit, the shared-memory
+ * carve-out (all of the unified L1 for the K-ary kernels, whose pinned levels
+ * live there) and the occupancy are set / queried once per kernel
+ * and shape, not per call.
  */
 int bs_lookup(const void* idx, const void* queries, uint64_t m, void* out, void* stream);
 
@@ -267,6 +279,12 @@ int bs_erase(const void* idx, const void* del_keys, uint64_t m, int del_sorted, 
 
 /* Library version / build string (arch, commit-independent). */
 const char* bs_version(void);
+
+/* Number of kernels this library has launched on its lookup paths (bs_lookup*,
+ * bs_lookup_host, bs_lookup_dist, bs_lookup_peer; not bs_build) since it was
+ * loaded, all threads and devices.  Read it before and after a region to count
+ * the region's launches (bench.py's gpu_launches). */
+uint64_t bs_launch_count(void);
 
 /* ------------------------------------------------------------------------
  * Multi-GPU (one process per GPU; BASELINE.json configs 4-5, not in the

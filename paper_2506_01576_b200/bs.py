@@ -24,7 +24,7 @@ HEADER = os.path.join(os.path.dirname(_HERE), "include", "bs.h")
 BS_OK, BS_ERR_INVALID, BS_ERR_UNSUPPORTED, BS_ERR_OOM, BS_ERR_CUDA, BS_ERR_NCCL, BS_ERR_NOT_SORTED = 0, -1, -2, -3, -4, -5, -6
 NAIVE, OPT, KARY = 0, 1, 2
 DYNAMIC, STATIC = 0, 1
-REORDER_NONE, REORDER_LOOKUP, REORDER_FULL = 0, 1, 2
+REORDER_NONE, REORDER_LOOKUP, REORDER_FULL, REORDER_SORTED = 0, 1, 2, 3
 HINT_STREAM_EVICT_FIRST, HINT_LEAF_EVICT_FIRST, HINT_SEP_EVICT_LAST = 1, 2, 4
 EXPORT_SORTED, EXPORT_PINNED, EXPORT_KARY = 0, 1, 2
 DIST_REPLICATED, DIST_PARTITIONED = 0, 1
@@ -88,6 +88,8 @@ def lib():
         L.bs_destroy.restype = None
         L.bs_last_error.restype = ctypes.c_char_p
         L.bs_version.restype = ctypes.c_char_p
+        L.bs_launch_count.restype = _u64
+        L.bs_launch_count.argtypes = []
         L.bs_index_info.argtypes = [vp, ctypes.POINTER(bs_info)]
         L.bs_export.argtypes = [vp, i, vp, _u64, ctypes.POINTER(_u64)]
         L.bs_dist_get_uid.argtypes = [vp]
@@ -132,6 +134,10 @@ def bs_last_error() -> str:
 
 def bs_version() -> str:
     return lib().bs_version().decode()
+
+
+def bs_launch_count() -> int:
+    return int(lib().bs_launch_count())
 
 
 def _ptr(x) -> int:

@@ -4,8 +4,10 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 #include <string>
+#include <unordered_map>
 
 #include "bs.h"
 #include "index.h"
@@ -13,6 +15,9 @@
 namespace bs {
 
 static thread_local std::string g_err;
+static std::atomic<uint64_t> g_launches{0};
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 int fail(int code, const char* fmt, ...) {
     char buf[512];
@@ -33,6 +38,78 @@ static bool reserved_zero(const uint32_t* r, int cnt) {
     for (int i = 0; i < cnt; ++i)
         if (r[i]) return false;
     return true;
+}
+
+// true if p is device (or managed) memory of `device`: bs_lookup takes GPU-resident
+// buffers only ("all data GPU-resident"); a host pointer would fault
+// asynchronously inside the kernel.  One driver query per buffer and call
+// (a host-side table lookup, well under the launch overhead).
+bool device_accessible(const void* p, int device) {
+    cudaPointerAttributes pa;
+    if (cudaPointerGetAttributes(&pa, p) != cudaSuccess) { cudaGetLastError(); return false; }
+    if (pa.type == cudaMemoryTypeManaged) return true;
+    return pa.type == cudaMemoryTypeDevice && pa.device == device;
+}
+
+// ---- launch planning (params.h plan_grid) ----
+namespace {
+struct KernelEntry {
+    int max_threads = 0;
+    int smem_set = -1;        // dynamic shared memory limit set so far
+    int carve_set = -1;       // carve-out set so far
+    uint32_t occ_threads = 0, occ_smem = 0;
+    int occ = -1;             // occupancy of (occ_threads, occ_smem)
+};
+std::mutex g_plan_mu;
+std::unordered_map<uint64_t, std::unordered_map<const void*, KernelEntry>> g_plans;   // device -> kernel
+}  // namespace
+
+cudaError_t plan_grid(const void* kern, uint32_t threads, uint32_t smem, Grid grid, uint64_t need, int carveout_pct,
+                      uint64_t* blocks, bool* uns) {
+    *blocks = 0;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(g_plan_mu);
+    KernelEntry& k = g_plans[(uint64_t)dev][kern];
+    if (k.max_threads == 0) {
+        cudaFuncAttributes fa;
+        e = cudaFuncGetAttributes(&fa, kern);
+        if (e != cudaSuccess) return e;
+        k.max_threads = fa.maxThreadsPerBlock;
+    }
+    if ((int)threads > k.max_threads || threads == 0 || threads % 32) { *uns = true; return cudaSuccess; }
+    if ((int)smem > k.smem_set) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        k.smem_set = (int)smem;
+    }
+    if (carveout_pct >= 0 && carveout_pct != k.carve_set) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carveout_pct);
+        if (e != cudaSuccess) return e;
+        k.carve_set = carveout_pct;
+        k.occ = -1;
+    }
+    uint64_t g = need;
+    if (grid.sched_static) {
+        int occ = (int)grid.ctas_per_sm;
+        if (occ == 0) {
+            if (k.occ < 0 || k.occ_threads != threads || k.occ_smem != smem) {
+                e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&k.occ, kern, (int)threads, smem);
+                if (e != cudaSuccess) { k.occ = -1; return e; }
+                k.occ_threads = threads;
+                k.occ_smem = smem;
+            }
+            occ = k.occ;
+        }
+        if (occ < 1) { *uns = true; return cudaSuccess; }
+        g = (uint64_t)grid.sm_count * (uint64_t)occ;
+    }
+    if (g > need) g = need;
+    if (g == 0) g = 1;
+    if (g > 0x7FFFFFFFull) g = 0x7FFFFFFFull;
+    *blocks = g;
+    return cudaSuccess;
 }
 
 static bool is_pow2(uint64_t x) { return x && !(x & (x - 1)); }
@@ -234,6 +311,8 @@ extern "C" {
 
 const char* bs_last_error(void) { return g_err.c_str(); }
 
+uint64_t bs_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
 const char* bs_version(void) {
     return "libbs 0.1 (sm_100a; naive / opt / kary; arXiv 2506.01576)";
 }
@@ -278,7 +357,7 @@ int bs_build(const void* keys, uint64_t n, const bs_layout* layout_in, void** ou
     if (lay.out_bytes == 4 && n >= (1ull << 31)) return fail(BS_ERR_INVALID, "out_bytes = 4 requires n < 2^31");
     if (lay.variant > BS_VARIANT_KARY) return fail(BS_ERR_INVALID, "unknown variant %u", lay.variant);
     if (lay.schedule > BS_SCHED_STATIC) return fail(BS_ERR_INVALID, "unknown schedule %u", lay.schedule);
-    if (lay.reorder > BS_REORDER_FULL) return fail(BS_ERR_INVALID, "unknown reorder %u", lay.reorder);
+    if (lay.reorder > BS_REORDER_SORTED) return fail(BS_ERR_INVALID, "unknown reorder %u", lay.reorder);
     if (lay.kary_mode > BS_KARY_MODE_AUTO) return fail(BS_ERR_INVALID, "unknown kary_mode %u", lay.kary_mode);
     if (lay.k < 2 || lay.k > 33) return fail(BS_ERR_INVALID, "K must be in [2, 33]");
     if (lay.leaf_chunk != 0 && (!is_pow2(lay.leaf_chunk) || lay.leaf_chunk > 256))
@@ -290,6 +369,9 @@ int bs_build(const void* keys, uint64_t n, const bs_layout* layout_in, void** ou
     const bool adopt = t_adopt_keys != nullptr && t_adopt_keys == keys && lay.input_sorted;
     t_adopt_keys = nullptr;
     Index* ix = new Index();
+    // an adopted buffer (bs_merge / bs_erase) is the index's from here on, so
+    // every failure path below frees it through free_index
+    if (adopt) ix->d_keys = const_cast<void*>(keys);
     ix->layout = lay;
     ix->n = n;
     ix->kb = lay.key_bytes;
@@ -331,9 +413,7 @@ int bs_build(const void* keys, uint64_t n, const bs_layout* layout_in, void** ou
 
     // ---- the sorted array ----
     // +256 keys of MAX padding: leaf chunks (C <= 256) may be read whole with vector loads
-    if (adopt) {
-        ix->d_keys = const_cast<void*>(keys);   // bs_merge's merged buffer: owned by the index from here on
-    } else {
+    if (!adopt) {
         e = cudaMalloc(&ix->d_keys, abytes + 256 * ix->kb + 16);
         if (e != cudaSuccess) { rc = fail_cuda(e, "cudaMalloc(keys)"); goto done; }
     }
@@ -466,12 +546,16 @@ int bs_lookup_ex(const void* idx, const void* queries, uint64_t m, void* out, vo
         bs_launch_default(idx, &L);
     }
     if (L.kary_mode > 7) return fail(BS_ERR_INVALID, "bs_lookup: unknown kary_mode %u", L.kary_mode);
+    if (L.reorder > BS_REORDER_SORTED) return fail(BS_ERR_INVALID, "bs_lookup: unknown reorder %u", L.reorder);
     if (m == 0) return BS_OK;
     if (!queries || !out) return fail(BS_ERR_INVALID, "bs_lookup: NULL queries/out with m > 0");
     const uintptr_t q0 = (uintptr_t)queries, q1 = q0 + m * ix->kb;
     const uintptr_t o0 = (uintptr_t)out, o1 = o0 + m * ix->ob;
     if (q0 < o1 && o0 < q1) return fail(BS_ERR_INVALID, "bs_lookup: out overlaps queries");
     if (q0 % ix->kb || o0 % ix->ob) return fail(BS_ERR_INVALID, "bs_lookup: misaligned queries/out");
+    if (!device_accessible(queries, ix->device) || !device_accessible(out, ix->device))
+        return fail(BS_ERR_INVALID, "bs_lookup: queries/out must be device memory of the index's GPU "
+                                    "(host buffers: bs_lookup_host)");
     return dispatch_lookup(ix, queries, m, out, (cudaStream_t)stream, L);
 }
 

@@ -6,6 +6,9 @@
 
 namespace bs {
 
+// host: counts this library's kernel launches on the lookup paths (bs_launch_count)
+void count_launch();
+
 template <class K> struct KeyMax;
 template <> struct KeyMax<uint32_t> { static constexpr uint32_t v = 0xFFFFFFFFu; };
 template <> struct KeyMax<uint64_t> { static constexpr uint64_t v = 0xFFFFFFFFFFFFFFFFull; };

@@ -40,14 +40,15 @@ struct DistState {
 #endif
     int P = 1, rank = 0;
     uint64_t max_m = 0;
+    uint64_t recv_cap = 0;            // sum of every rank's max_m_local (receive buffer slots)
     std::vector<uint64_t> base;       // global rank of each shard's first key
     void* d_shard_max = nullptr;      // P keys (u64 storage)
     uint8_t* d_dest = nullptr;        // per query destination
     uint32_t* d_perm = nullptr;       // per query slot in the send buffer
     uint64_t* d_counts = nullptr;     // P (mine) + P*P (gathered) + P cursors
     void* d_sendq = nullptr;          // max_m keys
-    void* d_recvq = nullptr;          // P * max_m keys
-    uint64_t* d_recvres = nullptr;    // P * max_m results
+    void* d_recvq = nullptr;          // recv_cap keys
+    uint64_t* d_recvres = nullptr;    // recv_cap results
     uint64_t* d_backres = nullptr;    // max_m results
 };
 
@@ -219,25 +220,30 @@ int bs_build_dist(void* comm, const void* local_keys, uint64_t n_local, int mode
     const uint32_t kb = ix->kb;
     cudaError_t e;
     auto cleanup = [&](int code) { bs_destroy(ix); *out_idx = nullptr; return code; };
-    // (min, max, n) of every shard
+    // (min, max, n, max_m_local) of every shard: every rank sizes its receive
+    // buffers from the SUM of all ranks' max_m_local, so a receive can never
+    // overflow and no rank ever has to leave a collective early
+    constexpr int NM = 4;
     uint64_t* d_meta = nullptr;
-    e = cudaMalloc(&d_meta, sizeof(uint64_t) * 3 * (P + 1));
+    e = cudaMalloc(&d_meta, sizeof(uint64_t) * NM * (P + 1));
     if (e != cudaSuccess) return cleanup(fail_cuda(e, "cudaMalloc(meta)"));
-    uint64_t mine[3] = {ix->a_first, ix->a_last, n_local};
+    uint64_t mine[NM] = {ix->a_first, ix->a_last, n_local, max_m_local};
     cudaMemcpy(d_meta, mine, sizeof mine, cudaMemcpyHostToDevice);
-    ncclResult_t r = ncclAllGather(d_meta, d_meta + 3, 3, ncclUint64, c->comm, 0);
+    ncclResult_t r = ncclAllGather(d_meta, d_meta + NM, NM, ncclUint64, c->comm, 0);
     if (r != ncclSuccess) { cudaFree(d_meta); return cleanup(nccl_fail(r, "ncclAllGather(meta)")); }
-    std::vector<uint64_t> meta(3 * P);
-    e = cudaMemcpy(meta.data(), d_meta + 3, sizeof(uint64_t) * 3 * P, cudaMemcpyDeviceToHost);
+    std::vector<uint64_t> meta(NM * P);
+    e = cudaMemcpy(meta.data(), d_meta + NM, sizeof(uint64_t) * NM * P, cudaMemcpyDeviceToHost);
     cudaFree(d_meta);
     if (e != cudaSuccess) return cleanup(fail_cuda(e, "meta copy"));
     d->base.assign(P, 0);
     uint64_t acc = 0;
+    d->recv_cap = 0;
     for (int s = 0; s < P; ++s) {
         d->base[s] = acc;
-        acc += meta[3 * s + 2];
+        acc += meta[NM * s + 2];
+        d->recv_cap += meta[NM * s + 3];
         if (s + 1 < P) {
-            const uint64_t mx = meta[3 * s + 1], mn_next = meta[3 * (s + 1)];
+            const uint64_t mx = meta[NM * s + 1], mn_next = meta[NM * (s + 1)];
             const bool ok = kb == 8 ? mx <= mn_next : (uint32_t)mx <= (uint32_t)mn_next;
             if (!ok) return cleanup(fail(BS_ERR_NOT_SORTED, "PARTITIONED: max of shard %d > min of shard %d", s, s + 1));
         }
@@ -247,12 +253,13 @@ int bs_build_dist(void* comm, const void* local_keys, uint64_t n_local, int mode
     if (e != cudaSuccess) return cleanup(fail_cuda(e, "cudaMalloc(shard_max)"));
     std::vector<uint64_t> mx64(P);
     std::vector<uint32_t> mx32(P);
-    for (int s = 0; s < P; ++s) { mx64[s] = meta[3 * s + 1]; mx32[s] = (uint32_t)meta[3 * s + 1]; }
+    for (int s = 0; s < P; ++s) { mx64[s] = meta[NM * s + 1]; mx32[s] = (uint32_t)meta[NM * s + 1]; }
     cudaMemcpy(d->d_shard_max, kb == 8 ? (void*)mx64.data() : (void*)mx32.data(), kb * P, cudaMemcpyHostToDevice);
     const uint64_t M = max_m_local ? max_m_local : 1;
+    const uint64_t R = d->recv_cap ? d->recv_cap : 1;
     struct { void** p; size_t b; } allocs[] = {
         {(void**)&d->d_dest, M}, {(void**)&d->d_perm, 4 * M}, {(void**)&d->d_counts, 8 * (size_t)(P * P + 3 * P)},
-        {&d->d_sendq, kb * M}, {&d->d_recvq, kb * M * P}, {(void**)&d->d_recvres, 8 * M * P},
+        {&d->d_sendq, kb * M}, {&d->d_recvq, kb * R}, {(void**)&d->d_recvres, 8 * R},
         {(void**)&d->d_backres, 8 * M}};
     for (auto& a : allocs) {
         e = cudaMalloc(a.p, a.b);
@@ -267,8 +274,12 @@ int bs_lookup_dist(const void* idx, const void* local_queries, uint64_t m_local,
     DistState* d = ix->dist;
     if (!d) return fail(BS_ERR_INVALID, "bs_lookup_dist: index was not built with bs_build_dist");
     if (d->mode == BS_DIST_REPLICATED) return bs_lookup(idx, local_queries, m_local, out_local, stream);
-    if (m_local > d->max_m) return fail(BS_ERR_INVALID, "bs_lookup_dist: m_local > max_m_local given at build");
-    if (m_local && (!local_queries || !out_local)) return fail(BS_ERR_INVALID, "bs_lookup_dist: NULL buffers");
+    // a bad call still takes part in every collective (with nothing to route),
+    // so the other ranks never wait on a rank that left early; it fails at the end
+    const char* bad = nullptr;
+    if (m_local > d->max_m) bad = "bs_lookup_dist: m_local > max_m_local given at build";
+    else if (m_local && (!local_queries || !out_local)) bad = "bs_lookup_dist: NULL buffers";
+    if (bad) m_local = 0;
     cudaStream_t s = (cudaStream_t)stream;
     const int P = d->P, me = d->rank;
     const uint32_t kb = ix->kb;
@@ -286,6 +297,7 @@ int bs_lookup_dist(const void* idx, const void* local_queries, uint64_t m_local,
         else
             k_route_count<uint32_t><<<grid_of(m_local), 256, 0, s>>>((const uint32_t*)local_queries, m_local,
                                                                      (const uint32_t*)d->d_shard_max, P, d->d_dest, cnt);
+        count_launch();
     }
     ncclResult_t r = ncclAllGather(cnt, all, P, ncclUint64, comm, s);
     if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather(counts)");
@@ -303,7 +315,7 @@ int bs_lookup_dist(const void* idx, const void* local_queries, uint64_t m_local,
         roff[t] = racc;
         racc += rcnt[t];
     }
-    if (racc > d->max_m * (uint64_t)P) return fail(BS_ERR_INVALID, "bs_lookup_dist: receive overflow");
+    // racc <= sum of every rank's m_local <= sum of max_m_local = recv_cap (sized at build)
     e = cudaMemcpyAsync(offs, soff.data(), sizeof(unsigned long long) * P, cudaMemcpyHostToDevice, s);
     if (e != cudaSuccess) return fail_cuda(e, "dist offsets");
     const uint64_t sc_tiles = (m_local + kScatterTile - 1) / kScatterTile;
@@ -317,6 +329,7 @@ int bs_lookup_dist(const void* idx, const void* local_queries, uint64_t m_local,
             k_route_scatter<uint32_t><<<grid_scatter, kScatterThreads, 0, s>>>((const uint32_t*)local_queries, m_local,
                                                                              d->d_dest, offs, cur, (uint32_t*)d->d_sendq,
                                                                              d->d_perm, P);
+        count_launch();
     }
     const ncclDataType_t kt = kb == 8 ? ncclUint64 : ncclUint32;
     ncclGroupStart();
@@ -331,6 +344,7 @@ int bs_lookup_dist(const void* idx, const void* local_queries, uint64_t m_local,
         int rc = bs_lookup(idx, d->d_recvq, racc, d->d_recvres, s);
         if (rc != BS_OK) return rc;
         k_add_base<<<grid_of(racc), 256, 0, s>>>(d->d_recvres, racc, d->base[me]);
+        count_launch();
     }
     ncclGroupStart();
     for (int t = 0; t < P; ++t) {
@@ -340,9 +354,13 @@ int bs_lookup_dist(const void* idx, const void* local_queries, uint64_t m_local,
     }
     r = ncclGroupEnd();
     if (r != ncclSuccess) return nccl_fail(r, "result all-to-all");
-    if (m_local) k_unroute<<<grid_of(m_local), 256, 0, s>>>(d->d_backres, d->d_perm, m_local, (uint64_t*)out_local);
+    if (m_local) {
+        k_unroute<<<grid_of(m_local), 256, 0, s>>>(d->d_backres, d->d_perm, m_local, (uint64_t*)out_local);
+        count_launch();
+    }
     e = cudaGetLastError();
     if (e != cudaSuccess) return fail_cuda(e, "dist kernels");
+    if (bad) return fail(BS_ERR_INVALID, "%s", bad);
     return BS_OK;
 }
 

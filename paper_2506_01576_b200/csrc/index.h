@@ -1,6 +1,7 @@
 // index.h — the index object behind the opaque bs_index handle (internal).
 #pragma once
 #include <cstdint>
+#include <atomic>
 #include <mutex>
 
 #include <cuda_runtime.h>
@@ -87,7 +88,8 @@ struct Index {
     // device
     int sm_count = 148, smem_optin = 232448, smem_per_sm = 233472, l2_bytes = 0;
     double build_ms = 0;
-    mutable uint64_t last_opt_smem = 0, last_kary_smem = 0;
+    // shared memory of the last OPT / K-ary launch (bs_info; atomics: lookups may run concurrently)
+    mutable std::atomic<uint64_t> last_opt_smem{0}, last_kary_smem{0};
 
     // lazily created host-path context
     std::mutex host_mu;
@@ -99,6 +101,7 @@ struct Index {
 };
 
 int fail(int code, const char* fmt, ...);
+bool device_accessible(const void* p, int device);
 // set by bs_merge right before bs_build(merged, ...): the index adopts that
 // device buffer (n keys + 256 keys of padding + 16 B) instead of copying it;
 // the index owns it from then on, on success and on failure alike
@@ -111,6 +114,8 @@ int dispatch_lookup(const Index* ix, const void* q, uint64_t m, void* out, cudaS
 int dispatch_kary_peer(const Index* ix, const void* q, uint64_t cap, cudaStream_t s, const bs_launch& L,
                        const PeerLaunch& pl);
 uint32_t kary_smem_levels(const Index* ix, uint32_t* bytes_out, uint64_t cap_bytes = 0);
+// the layout can run the thread-per-lookup K-ary kernel (kary_mode 6/7), which holds the peer epilogue
+bool g1_shape_ok(const Index* ix);
 
 // host.cu / dist.cu
 void destroy_host_ctx(Index* ix);

@@ -96,7 +96,12 @@ k_kary_g1(const KaryParams<K> p, const K* __restrict__ q, uint64_t m_arg, void* 
 
     auto load_tile = [&](uint64_t t) -> K {
         const uint64_t i = t * 32 + lane;
-        return (t < nwt && i < m) ? load_stream(q + i, true, pol_stream) : KeyMax<K>::v;
+        if (t >= nwt || i >= m) return KeyMax<K>::v;
+        // PEER: the receive window is written by other GPUs while this kernel is
+        // resident (before the acquire in peer_wait_ge), so its queries are read
+        // with the coherent L2 path (ld.global.cg), never the non-coherent one
+        if constexpr (PEER) return __ldcg(q + i);
+        else return load_stream(q + i, true, pol_stream);
     };
 
     // T warp-tiles per iteration: each thread carries T independent lookups
@@ -389,7 +394,8 @@ k_kary_g1p(const KaryParams<K> p, const K* __restrict__ q, uint64_t m, void* __r
         // ---- global separator levels of tile t, next tile's probes in between ----
         for (uint32_t l = Ls; l < L; ++l) {
             K s[W];
-            ld_node<K, W>(p.sep + p.lvl_base[l] + (uint64_t)node * W, true, pol_sep, s);
+            // evict_last only for the levels that fit L2 (as k_kary_g1)
+            ld_node<K, W>(p.sep + p.lvl_base[l] + (uint64_t)node * W, true, l < p.sep_last_end ? pol_sep : pol_leaf, s);
             for (uint32_t r = 0; r < per && dn < D; ++r, ++dn) probe(kn, key_n, tie_n);
             uint32_t c = 0;
 #pragma unroll
@@ -460,27 +466,12 @@ static cudaError_t go_g1(const void* params, const void* q, uint64_t m, void* ou
     if (flat && T == 1 && !peer && ob == sizeof(K) && !runtime_ob)
         kern = k_kary_g1<K, W, GL, IL, 1, true, false, (int)sizeof(K)>;
     if (flat && T == 3 && !peer) kern = k_kary_g1p<K, W, GL, IL>;   // T = 3 encodes "pipelined, one lookup per thread"
-    cudaFuncAttributes fa;
-    cudaError_t e = cudaFuncGetAttributes(&fa, kern);
-    if (e != cudaSuccess) return e;
-    if ((int)threads > fa.maxThreadsPerBlock || threads % 32) { *uns = true; return cudaSuccess; }
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
     const uint64_t need = (m + threads - 1) / threads;
-    uint64_t g = need;
-    if (grid.sched_static) {
-        int occ = (int)grid.ctas_per_sm;
-        if (occ == 0) {
-            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, (int)threads, smem);
-            if (e != cudaSuccess) return e;
-        }
-        if (occ < 1) { *uns = true; return cudaSuccess; }
-        g = (uint64_t)grid.sm_count * (uint64_t)occ;
-    }
-    if (g > need) g = need;
-    if (g == 0) g = 1;
-    if (g > 0x7FFFFFFFull) g = 0x7FFFFFFFull;
+    uint64_t g = 0;
+    cudaError_t e = plan_grid((const void*)kern, threads, smem, grid, need, carveout_for(smem, threads), &g, uns);
+    if (e != cudaSuccess || *uns) return e;
     kern<<<(unsigned)g, threads, smem, s>>>(*(const KaryParams<K>*)params, (const K*)q, m, out, ob);
+    count_launch();
     return cudaGetLastError();
 }
 

@@ -179,28 +179,13 @@ template <class K, class O, int W, int I, int CPL>
 static cudaError_t go_hybrid(const void* params, const void* q, uint64_t m, void* out, uint32_t threads,
                              Grid grid, uint32_t smem, cudaStream_t s, bool* uns) {
     auto kern = k_kary_hybrid<K, O, W, I, CPL>;
-    cudaFuncAttributes fa;
-    cudaError_t e = cudaFuncGetAttributes(&fa, kern);
-    if (e != cudaSuccess) return e;
-    if ((int)threads > fa.maxThreadsPerBlock || threads % 32) { *uns = true; return cudaSuccess; }
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
     const uint64_t per_cta = (uint64_t)threads;   // one lookup per thread per tile
     const uint64_t need = (m + per_cta - 1) / per_cta;
-    uint64_t g = need;
-    if (grid.sched_static) {
-        int occ = (int)grid.ctas_per_sm;
-        if (occ == 0) {
-            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, (int)threads, smem);
-            if (e != cudaSuccess) return e;
-        }
-        if (occ < 1) { *uns = true; return cudaSuccess; }
-        g = (uint64_t)grid.sm_count * (uint64_t)occ;
-    }
-    if (g > need) g = need;
-    if (g == 0) g = 1;
-    if (g > 0x7FFFFFFFull) g = 0x7FFFFFFFull;
+    uint64_t g = 0;
+    cudaError_t e = plan_grid((const void*)kern, threads, smem, grid, need, carveout_for(smem, threads), &g, uns);
+    if (e != cudaSuccess || *uns) return e;
     kern<<<(unsigned)g, threads, smem, s>>>(*(const KaryParams<K>*)params, (const K*)q, m, (O*)out);
+    count_launch();
     return cudaGetLastError();
 }
 

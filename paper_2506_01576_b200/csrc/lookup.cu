@@ -290,6 +290,12 @@ static int run_kary(const Index* ix, const void* q, uint64_t m, void* out, cudaS
     return BS_OK;
 }
 
+bool g1_shape_ok(const Index* ix) {
+    const uint32_t W = ix->kW, C = ix->kC, kb = ix->kb;
+    return ix->kary_built && (ix->layout.kary_mode == 6 || ix->layout.kary_mode == 7) && W * kb <= 64 &&
+           W * kb >= 8 && C * kb >= 32 && C * kb <= 256;
+}
+
 int dispatch_kary_peer(const Index* ix, const void* q, uint64_t cap, cudaStream_t s, const bs_launch& L,
                        const PeerLaunch& pl) {
     if (L.variant != BS_VARIANT_KARY) return fail(BS_ERR_UNSUPPORTED, "bs_lookup_peer: needs variant KARY");
@@ -298,6 +304,16 @@ int dispatch_kary_peer(const Index* ix, const void* q, uint64_t cap, cudaStream_
 }
 
 int dispatch_lookup(const Index* ix, const void* q, uint64_t m, void* out, cudaStream_t s, const bs_launch& L) {
+    if (L.reorder == BS_REORDER_SORTED) {
+        // an ordered batch (Fig. 1b): segment-staged lookup, any variant's index
+        bool uns = false;
+        Grid g{1u, 1u, (uint32_t)ix->sm_count};
+        cudaError_t e = launch_seg_sorted(ix->kb, ix->ob, ix->d_keys, ix->n, q, m, out,
+                                          (L.cache_hints & BS_HINT_STREAM_EVICT_FIRST) ? 1u : 0u, g, s, &uns);
+        if (uns) return fail(BS_ERR_UNSUPPORTED, "BS_REORDER_SORTED: index too large for the segment table");
+        if (e != cudaSuccess) return fail_cuda(e, "segment lookup launch");
+        return BS_OK;
+    }
     switch (L.variant) {
         case BS_VARIANT_NAIVE: {
             cudaError_t e = launch_naive(ix->kb, ix->ob, ix->d_keys, ix->n, q, m, out, L.threads, s);

@@ -46,6 +46,7 @@ cudaError_t launch_naive(int kb, int ob, const void* a, uint64_t n, const void* 
         k_naive<uint32_t, uint64_t><<<g, b, 0, s>>>((const uint32_t*)a, n, (const uint32_t*)q, m, (uint64_t*)out);
     else
         k_naive<uint32_t, uint32_t><<<g, b, 0, s>>>((const uint32_t*)a, n, (const uint32_t*)q, m, (uint32_t*)out);
+    count_launch();
     return cudaGetLastError();
 }
 

@@ -219,27 +219,13 @@ template <class K, class O, int NREG, int RE>
 static cudaError_t go_opt(const void* params, const void* q, uint64_t m, void* out, uint32_t threads,
                           Grid grid, uint32_t smem, cudaStream_t s, bool* unsupported) {
     auto kern = k_bs_opt<K, O, NREG, RE>;
-    cudaFuncAttributes fa;
-    cudaError_t e = cudaFuncGetAttributes(&fa, kern);
-    if (e != cudaSuccess) return e;
-    if ((int)threads > fa.maxThreadsPerBlock) { *unsupported = true; return cudaSuccess; }
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
     const uint64_t tile = (uint64_t)threads * NREG;
     const uint64_t ntiles = (m + tile - 1) / tile;
-    uint64_t g = ntiles;
-    if (grid.sched_static) {
-        int occ = (int)grid.ctas_per_sm;
-        if (occ == 0) {
-            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, (int)threads, smem);
-            if (e != cudaSuccess) return e;
-        }
-        if (occ < 1) { *unsupported = true; return cudaSuccess; }
-        g = (uint64_t)grid.sm_count * (uint64_t)occ;
-    }
-    if (g > ntiles) g = ntiles;
-    if (g > 0x7FFFFFFFull) g = 0x7FFFFFFFull;
+    uint64_t g = 0;
+    cudaError_t e = plan_grid((const void*)kern, threads, smem, grid, ntiles, carveout_for(smem, threads), &g, unsupported);
+    if (e != cudaSuccess || *unsupported) return e;
     kern<<<(unsigned)g, threads, smem, s>>>(*(const OptParams<K>*)params, (const K*)q, m, (O*)out);
+    count_launch();
     return cudaGetLastError();
 }
 

@@ -83,14 +83,56 @@ struct KaryParams {
     uint32_t peer_shift;
 };
 
+// Segment-staged lookup of an ordered batch (seg.cu, BS_REORDER_SORTED)
+template <class K>
+struct SegParams {
+    const K* a;              // sorted array
+    uint64_t n;
+    const K* q;              // queries (any order; fast when ascending)
+    uint64_t m;
+    void* out;
+    uint32_t ob;
+    uint64_t B;              // segments of 2^kSegLog2 keys = ceil(n / S)
+    uint32_t stream_hint;    // queries / results with L2 evict_first
+};
+
 // ---- launchers (return cudaGetLastError() after the launch) ----
 cudaError_t launch_naive(int kb, int ob, const void* a, uint64_t n, const void* q, uint64_t m,
                          void* out, uint32_t threads, cudaStream_t s);
+
 
 // Grid: sched_static = 0 -> dynamic (one tile / warp-tile set per CTA on the
 // hardware scheduler); 1 -> persistent grid of sm_count x ctas_per_sm CTAs
 // (ctas_per_sm = 0: as many as are co-resident, from the occupancy API).
 struct Grid { uint32_t sched_static, ctas_per_sm, sm_count; };
+
+cudaError_t launch_seg_sorted(int kb, int ob, const void* a, uint64_t n, const void* q, uint64_t m, void* out,
+                              uint32_t stream_hint, Grid grid, cudaStream_t s, bool* uns);
+
+// Shared-memory carve-out of a kernel (cudaFuncAttributePreferredSharedMemoryCarveout,
+// percent of the SM's 228 KB unified L1/shared array): the smallest that holds the
+// resident CTAs' shared memory; the rest stays L1.  Even the K-ary kernels, whose
+// global loads do not allocate in L1, need it: L1 also receives the data of every
+// load in flight, and a random lookup lives on loads in flight (measured on config
+// 3: carve-out 100 % -> 4.99 ms, smallest fitting -> 3.87 ms).
+inline int carveout_for(uint32_t smem, uint32_t threads) {
+    const uint64_t cap = 228u * 1024u, per = (uint64_t)smem + 1024u;
+    uint64_t ctas = 2048u / (threads ? threads : 1u);          // resident CTAs the threads allow
+    if (ctas * per > cap) ctas = cap / per;                     // ... and the shared memory
+    if (ctas < 1) ctas = 1;
+    uint64_t need = ctas * per;
+    if (need > cap) need = cap;
+    const uint64_t pct = (100u * need + cap - 1) / cap;
+    return (int)(pct < 1 ? 1 : pct);
+}
+
+// Grid of a lookup launch: `need` blocks of work, or the persistent grid
+// (SMs x occupancy) for the static schedule.  The kernel's attributes are queried
+// once per (device, kernel); the dynamic-shared-memory limit and the carve-out are
+// set only when they change; the occupancy of the last (threads, smem) shape is
+// cached.  *uns = true (and no error) if the shape cannot launch.
+cudaError_t plan_grid(const void* kern, uint32_t threads, uint32_t smem, Grid grid, uint64_t need, int carveout_pct,
+                      uint64_t* blocks, bool* uns);
 
 cudaError_t launch_opt(int kb, int ob, const void* params, const void* q, uint64_t m, void* out,
                        uint32_t threads, uint32_t nreg, uint32_t reorder, Grid grid,

@@ -248,6 +248,13 @@ int bs_build_peer(const void* local_keys, uint64_t n_local, const bs_layout* lay
     if (ix->ob != 8) return cleanup(fail(BS_ERR_INVALID, "bs_build_peer: needs out_bytes = 8 (global ranks)"));
     if (ix->layout.variant != BS_VARIANT_KARY)
         return cleanup(fail(BS_ERR_UNSUPPORTED, "bs_build_peer: needs variant KARY (the g1 kernel carries the peer epilogue)"));
+    // reject, after the AUTO choices are resolved, every layout the g1 kernel cannot
+    // run: a lookup would otherwise fail only after its route kernel had already
+    // filled the peers' windows and bumped their counters
+    if (!g1_shape_ok(ix))
+        return cleanup(fail(BS_ERR_UNSUPPORTED, "bs_build_peer: layout needs kary_mode 6/7 with W*key <= 64 B and "
+                                                "C*key in 32..256 B (got mode %u, W %u, C %u, key %u B)",
+                            ix->layout.kary_mode, ix->kW, ix->kC, ix->kb));
     PeerState* d = new PeerState();
     ix->peer = d;
     d->P = world;
@@ -381,6 +388,7 @@ int bs_lookup_peer(const void* idx, const void* local_queries, uint64_t m_local,
     if (m_local && !local_queries) return fail(BS_ERR_INVALID, "bs_lookup_peer: NULL queries");
     if ((uintptr_t)local_queries % ix->kb || (uintptr_t)out_local % 8)
         return fail(BS_ERR_INVALID, "bs_lookup_peer: misaligned queries/out");
+    if (!g1_shape_ok(ix)) return fail(BS_ERR_UNSUPPORTED, "bs_lookup_peer: layout cannot run the g1 kernel");
     cudaStream_t s = (cudaStream_t)stream;
     const uint32_t P = (uint32_t)d->P, me = (uint32_t)d->rank;
     PeerCtl* c = d->ctl();
@@ -393,6 +401,7 @@ int bs_lookup_peer(const void* idx, const void* local_queries, uint64_t m_local,
     else
         k_peer_route<uint32_t><<<gr, 256, 0, s>>>((const uint32_t*)local_queries, m_local, d->d_peers, d->d_shard_max, P,
                                                   me, tag_shift(P), d->cap, &c->done_route, &c->err);
+    count_launch();
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail_cuda(e, "k_peer_route launch");
     bs_launch L;
@@ -408,6 +417,7 @@ int bs_lookup_peer(const void* idx, const void* local_queries, uint64_t m_local,
     const uint64_t mc = out_local ? m_local : 0;
     k_peer_finish<<<grid_for(mc / 2, (unsigned)ix->sm_count * 8), 256, 0, s>>>(
         (const uint64_t*)(d->region + d->lay.ret), mc, (uint64_t*)out_local, &c->ret_sig, target, &c->err);
+    count_launch();
     e = cudaGetLastError();
     if (e != cudaSuccess) return fail_cuda(e, "k_peer_finish launch");
     return BS_OK;

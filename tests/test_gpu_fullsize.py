@@ -48,12 +48,21 @@ def _check_invariant(dk, dq, out, n, kb):
     assert bool((hit == ~miss).all()), "hit bit wrong"
 
 
+def _inputs(cfg, order, m_cap=1 << 27):
+    """bench.py's inputs (workload/device.py on the GPU, rank 0 of 1); config 4's
+    batch is capped at 2^27 queries (its per-GPU share at 8 GPUs)."""
+    dk, dq, _ = bench._gen(cfg, 0, 1, "strong", order, "cuda")
+    dq = dq[:m_cap].contiguous()
+    kb = dk.element_size()
+    return dk, dq, bench._host(dk, kb), bench._host(dq, kb)
+
+
 @pytest.mark.parametrize("cfg,order", [("config2", "random"), ("config3", "random"), ("config3", "sorted"),
                                        ("config4", "random")])
 def test_fullsize_bench_launch(cfg, order):
-    n, kb, m, hr, _ = bench.CONFIGS[cfg]
-    keys, q, _ = bench.make_inputs(cfg, order, 0)
-    dk, dq = P.as_torch(keys), P.as_torch(q)
+    n, kb = bench.CONFIGS[cfg][:2]
+    dk, dq, keys, q = _inputs(cfg, order)
+    m = q.size
     out = torch.empty(m, dtype={4: torch.int32, 8: torch.int64}[kb], device="cuda")
     # bench.py's launch configuration: the layout defaults (K, C, kary_mode, threads, nreg)
     lay = bs.bs_layout_default(key_bytes=kb, out_bytes=kb)
@@ -64,6 +73,30 @@ def test_fullsize_bench_launch(cfg, order):
     got = P.to_numpy_unsigned(out, kb)[samp]
     want = oracle.lookup(keys, q[samp], out_bytes=kb)
     assert np.array_equal(got, want)
+    _check_invariant(dk, dq, out, n, kb)
+    idx.close()
+    del dk, dq, out
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("variant", ["naive", "opt"])
+def test_fullsize_config3_naive_opt(variant):
+    """The naive Listing-1 kernel and the §4 OPT kernel at config-3 size: OPT's
+    deep-level evict_first branch (evict_step) and L1 upper levels are only
+    active when the array is far larger than L2."""
+    n, kb = bench.CONFIGS["config3"][:2]
+    dk, dq, keys, q = _inputs("config3", "random")
+    m = q.size
+    out = torch.empty(m, dtype=torch.int64, device="cuda")
+    lay = bs.bs_layout_default(key_bytes=kb, out_bytes=kb, variant=bench.VARIANTS[variant])
+    idx = bs.bs_build(dk, n, lay)
+    if variant == "opt":
+        bs.bs_lookup_ex(idx, dq, m, out, None, variant=bs.OPT, schedule=bs.STATIC, threads=256, nreg=8)
+    else:
+        bs.bs_lookup_ex(idx, dq, m, out, None, variant=bs.NAIVE, threads=256)
+    torch.cuda.synchronize()
+    samp = np.random.default_rng(12).integers(0, m, size=1 << 16)
+    assert np.array_equal(P.to_numpy_unsigned(out, kb)[samp], oracle.lookup(keys, q[samp], out_bytes=kb))
     _check_invariant(dk, dq, out, n, kb)
     idx.close()
     del dk, dq, out

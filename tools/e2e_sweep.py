@@ -22,7 +22,7 @@ from paper_2506_01576_b200 import bs  # noqa: E402
 
 torch.cuda.set_device(0)
 keys, q, _ = bench.make_inputs("config3", "random", 0)
-n, kb, m, _, _ = bench.CONFIGS["config3"]
+n, kb, m = bench.CONFIGS["config3"][:3]
 dk = P.as_torch(keys)
 hq = torch.from_numpy(q.view(np.int64)).pin_memory()
 hout = torch.empty(m, dtype=torch.int64).pin_memory()

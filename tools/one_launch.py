@@ -40,7 +40,7 @@ if a.l2fetch:
     rt.cudaFree(None)
     print("cudaDeviceSetLimit(L2 fetch) rc", rt.cudaDeviceSetLimit(ctypes.c_int(0x05), ctypes.c_size_t(a.l2fetch)))
 keys, q, _ = bench.make_inputs(a.config, a.order, 0)
-n, kb, m, _, _ = bench.CONFIGS[a.config]
+n, kb, m = bench.CONFIGS[a.config][:3]
 v = bench.VARIANTS[a.variant]
 idx = bs.bs_build(P.as_torch(keys), n, bs.bs_layout_default(key_bytes=kb, out_bytes=kb, variant=v, k=a.k,
                                                             leaf_chunk=a.c))

@@ -27,7 +27,7 @@ ap.add_argument("--pts", required=True)
 a = ap.parse_args()
 torch.cuda.set_device(0)
 keys, q, _ = bench.make_inputs(a.config, a.order, 0)
-n, kb, m, _, _ = bench.CONFIGS[a.config]
+n, kb, m = bench.CONFIGS[a.config][:3]
 dk, dq = P.as_torch(keys), P.as_torch(q)
 out = torch.empty(m, dtype={4: torch.int32, 8: torch.int64}[kb], device="cuda")
 pts = [list(map(int, x.split("/"))) for x in a.pts.split(",")]

@@ -56,7 +56,7 @@ def main():
     args = ap.parse_args()
     torch.cuda.set_device(0)
     keys, q, desc = bench.make_inputs(args.config, args.order, 0)
-    n, kb, m, _, _ = bench.CONFIGS[args.config]
+    n, kb, m = bench.CONFIGS[args.config][:3]
     dk, dq = P.as_torch(keys), P.as_torch(q)
     out = torch.empty(m, dtype={4: torch.int32, 8: torch.int64}[kb], device="cuda")
     samp = np.random.default_rng(7).integers(0, m, size=1 << 12)

@@ -171,7 +171,8 @@ def gen_keys_range(n: int, lo: int, hi: int, seed: int, shard: int, device="cuda
     got = None
     pos = 0
     while got is None or got.numel() < n:
-        extra = (n if got is None else n - got.numel()) * 2 + 64
+        # over-draw by twice the expected duplicates plus slack (as gen_keys)
+        extra = (n + (2 * n * n >> (width.bit_length() - 1)) + 64) if got is None else (n - got.numel()) * 2 + 64
         v = hash_stream(seed, 16 + shard, pos, extra, device)
         pos += extra
         if sh == 64:
