@@ -493,9 +493,14 @@ def main():
             bs.bs_lookup_peer(idx, dq, m, out, stream)
     else:
         idx = bs.bs_build(dk, n_loc, lay)
+        ws_bytes = bs.bs_workspace_bytes(idx, m)   # BS_REORDER_GLOBAL partitions out of place
+        ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device="cuda") if ws_bytes else None
 
         def step():
-            bs.bs_lookup(idx, dq, m, out, stream)
+            if ws is not None:
+                bs.bs_lookup_ws(idx, dq, m, out, stream, ws, ws_bytes)
+            else:
+                bs.bs_lookup(idx, dq, m, out, stream)
     info = idx.info
     launch = bs.bs_launch_default(idx)
     say("index built", info)
@@ -546,7 +551,7 @@ def main():
     naive_ms = None
     if not args.no_naive and args.variant != "naive" and mode == "replicated":
         def step_naive():
-            bs.bs_lookup_ex(idx, dq, m, out, stream, variant=bs.NAIVE, threads=256)
+            bs.bs_lookup_ex(idx, dq, m, out, stream, variant=bs.NAIVE, threads=256, reorder=0)
         ns = max(1, min(args.steps, 5 if m <= (1 << 27) else 1))
         nms, _, _ = timed(step_naive, ns)
         naive_ms = reduce_max([nms / ns], world, "cuda")[0]

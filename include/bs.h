@@ -60,12 +60,17 @@ typedef enum {
     BS_REORDER_LOOKUP = 1, /* §4.3 "lookup-reordering": block-local sort, direct stores */
     BS_REORDER_FULL = 2,   /* §4.3 "full-reordering": + inverse permutation before a coalesced
                               store (Listing 2 l.35-39)                                 */
-    BS_REORDER_SORTED = 3  /* the batch is ordered (Fig. 1b): segment-staged lookup —
+    BS_REORDER_SORTED = 3, /* the batch is ordered (Fig. 1b): segment-staged lookup —
                               per segment of 8192 keys one CTA stages a 32-bit order-preserving
                               image in shared memory and searches its share of the (sorted)
                               batch there.  Any variant's index.  Correct for ANY batch order
                               (queries outside their segment's range take a global
                               bisection); fast only when the batch is ascending.             */
+    BS_REORDER_GLOBAL = 4  /* the batch is reordered GLOBALLY (the paper's out-of-place reference
+                              point): one partition pass groups the queries by the
+                              8192-key segment that holds their answer (records in a caller
+                              workspace), the segment-staged lookup runs per segment, one pass
+                              restores query order.  Needs bs_lookup_ws; n <= 2^27 keys.     */
 } bs_reorder;
 
 /* Build-time structure + default launch configuration.
@@ -86,7 +91,7 @@ typedef struct {
                                kept in shared memory (§5.1); 0 = no pinning;
                                0xFFFFFFFF = largest that fits                              */
     uint32_t pin_partial;   /* OPT: 1 = "full-pinning" (partial step M+1), 0 = "steps-pinning" */
-    uint32_t reorder;       /* bs_reorder: 1-2 OPT only; 3 (SORTED) any variant             */
+    uint32_t reorder;       /* bs_reorder: 1-2 OPT only; 3 (SORTED), 4 (GLOBAL) any variant */
     uint32_t k;             /* KARY fan-out K, 2..33 (P:223 A6000 best K = 17)       */
     uint32_t leaf_chunk;    /* KARY leaf chunk C in keys, power of two 1..256; 0 =
                                auto (layout default), resolved by bs_build: the smallest
@@ -241,6 +246,24 @@ int bs_lookup_ex(const void* idx, const void* queries, uint64_t m, void* out, vo
  */
 int bs_lookup_host(const void* idx, const void* host_queries, uint64_t m, void* host_out,
                    void* stream);
+
+/*
+ * Workspace-taking lookup (the BS_REORDER_GLOBAL mode, which partitions the
+ * batch out of place).
+ *   bs_workspace_bytes: *bytes = device bytes a bs_lookup_ws call with this
+ *     launch (NULL = index defaults) needs for m queries (0 if the mode needs
+ *     none).  BS_ERR_UNSUPPORTED if the mode cannot run on this index (GLOBAL:
+ *     n > 2^27 keys, or m >= 2^32).
+ *   bs_lookup_ws: bs_lookup_ex plus a caller-owned device workspace `ws` of
+ *     ws_bytes (no allocation inside; the workspace must not be shared by calls
+ *     in flight on other streams).  BS_ERR_INVALID if ws is NULL / too small for
+ *     a mode that needs one.  Other modes ignore ws.  Same result contract.
+ * bs_lookup / bs_lookup_ex with reorder = BS_REORDER_GLOBAL return
+ * BS_ERR_INVALID (no workspace).
+ */
+int bs_workspace_bytes(const void* idx, uint64_t m, const bs_launch* launch, uint64_t* bytes);
+int bs_lookup_ws(const void* idx, const void* queries, uint64_t m, void* out, void* stream, const bs_launch* launch,
+                 void* ws, uint64_t ws_bytes);
 
 /* Frees everything the index owns.  NULL-safe.  No lookups may be in flight. */
 void bs_destroy(void* idx);

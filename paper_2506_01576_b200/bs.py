@@ -24,7 +24,7 @@ HEADER = os.path.join(os.path.dirname(_HERE), "include", "bs.h")
 BS_OK, BS_ERR_INVALID, BS_ERR_UNSUPPORTED, BS_ERR_OOM, BS_ERR_CUDA, BS_ERR_NCCL, BS_ERR_NOT_SORTED = 0, -1, -2, -3, -4, -5, -6
 NAIVE, OPT, KARY = 0, 1, 2
 DYNAMIC, STATIC = 0, 1
-REORDER_NONE, REORDER_LOOKUP, REORDER_FULL, REORDER_SORTED = 0, 1, 2, 3
+REORDER_NONE, REORDER_LOOKUP, REORDER_FULL, REORDER_SORTED, REORDER_GLOBAL = 0, 1, 2, 3, 4
 HINT_STREAM_EVICT_FIRST, HINT_LEAF_EVICT_FIRST, HINT_SEP_EVICT_LAST = 1, 2, 4
 EXPORT_SORTED, EXPORT_PINNED, EXPORT_KARY = 0, 1, 2
 DIST_REPLICATED, DIST_PARTITIONED = 0, 1
@@ -84,6 +84,8 @@ def lib():
         L.bs_lookup.argtypes = [vp, vp, _u64, vp, vp]
         L.bs_lookup_ex.argtypes = [vp, vp, _u64, vp, vp, ctypes.POINTER(bs_launch)]
         L.bs_lookup_host.argtypes = [vp, vp, _u64, vp, vp]
+        L.bs_lookup_ws.argtypes = [vp, vp, _u64, vp, vp, ctypes.POINTER(bs_launch), vp, _u64]
+        L.bs_workspace_bytes.argtypes = [vp, _u64, ctypes.POINTER(bs_launch), ctypes.POINTER(_u64)]
         L.bs_destroy.argtypes = [vp]
         L.bs_destroy.restype = None
         L.bs_last_error.restype = ctypes.c_char_p
@@ -109,7 +111,8 @@ def lib():
         for f in ("bs_layout_default", "bs_launch_default", "bs_build", "bs_lookup", "bs_lookup_ex",
                   "bs_lookup_host", "bs_index_info", "bs_export", "bs_dist_get_uid", "bs_dist_init",
                   "bs_build_dist", "bs_lookup_dist", "bs_build_peer", "bs_peer_export", "bs_peer_connect",
-                  "bs_lookup_peer", "bs_peer_status", "bs_peer_results", "bs_merge", "bs_erase"):
+                  "bs_lookup_peer", "bs_peer_status", "bs_peer_results", "bs_merge", "bs_erase",
+                  "bs_lookup_ws", "bs_workspace_bytes"):
             getattr(L, f).restype = i
         _lib = L
     return _lib
@@ -217,6 +220,29 @@ def bs_lookup_ex(index: Index, queries, m: int, out, stream=None, launch: bs_lau
         setattr(launch, k, v)
     return _check(lib().bs_lookup_ex(index.handle, _ptr(queries), m, _ptr(out), _stream_ptr(stream),
                                      ctypes.byref(launch)))
+
+
+def _launch(index: Index, launch, over):
+    if launch is None:
+        launch = bs_launch_default(index)
+    for k, v in over.items():
+        setattr(launch, k, v)
+    return launch
+
+
+def bs_workspace_bytes(index: Index, m: int, launch: bs_launch | None = None, **over) -> int:
+    n = _u64()
+    _check(lib().bs_workspace_bytes(index.handle, m, ctypes.byref(_launch(index, launch, over)), ctypes.byref(n)))
+    return n.value
+
+
+def bs_lookup_ws(index: Index, queries, m: int, out, stream=None, ws=None, ws_bytes: int | None = None,
+                 launch: bs_launch | None = None, **over):
+    """ws: a device buffer (torch tensor) of at least bs_workspace_bytes(...) bytes."""
+    if ws_bytes is None:
+        ws_bytes = ws.numel() * ws.element_size() if ws is not None else 0
+    return _check(lib().bs_lookup_ws(index.handle, _ptr(queries), m, _ptr(out), _stream_ptr(stream),
+                                     ctypes.byref(_launch(index, launch, over)), _ptr(ws), ws_bytes))
 
 
 def bs_lookup_host(index: Index, host_queries, m: int, host_out, stream=None):

@@ -281,7 +281,18 @@ static int build_kary_layout(Index* ix, cudaStream_t st) {
             e = cudaMalloc(&ix->d_flat64, 8ull << D);
             if (e != cudaSuccess) return fail_cuda(e, "cudaMalloc(flat table 64)");
         }
-        e = build_flat_table(kb, ix->d_keys, n, span, ix->flat_M, D, ix->d_flat, ix->d_flat64, st);
+        if (kb == 8) {
+            // order-preserving 32-bit image: the array's span in 32 bits (keys < 2^32 exact)
+            e = cudaStreamSynchronize(st);   // a_first / a_last are on the host
+            if (e != cudaSuccess) return fail_cuda(e, "flat image range");
+            const uint64_t span_keys = ix->a_last - ix->a_first;
+            uint32_t bl = 0;
+            for (uint64_t x = span_keys; x; x >>= 1) ++bl;
+            ix->flat_fbase = ix->a_first;
+            ix->flat_fshift = bl > 32 ? bl - 32 : 0;
+        }
+        e = build_flat_table(kb, ix->d_keys, n, span, ix->flat_M, D, ix->d_flat, ix->d_flat64, ix->flat_fbase,
+                             ix->flat_fshift, st);
         if (e != cudaSuccess) return fail_cuda(e, "build_flat_table");
         // the flat level's node image next to the table (one buffer, one TMA
         // stage): mode 7 then descends one shared level below the table
@@ -292,9 +303,12 @@ static int build_kary_layout(Index* ix, cudaStream_t st) {
                 e = cudaMalloc(&ix->d_flatimg, ((1ull << D) + wl) * 4);
                 if (e != cudaSuccess) return fail_cuda(e, "cudaMalloc(flat table + level image)");
                 e = cudaMemcpyAsync(ix->d_flatimg, ix->d_flat, 4ull << D, cudaMemcpyDeviceToDevice, st);
-                if (e == cudaSuccess)
-                    e = cudaMemcpyAsync((uint32_t*)ix->d_flatimg + (1ull << D), (const uint32_t*)ix->d_img + ix->img_base[lt],
-                                        wl * 4, cudaMemcpyDeviceToDevice, st);
+                if (e == cudaSuccess) {
+                    const uint32_t* hi = (const uint32_t*)ix->d_img + ix->img_base[lt];
+                    const uint32_t* lo = kb == 8 ? hi + ix->img_base[ix->img_L] : nullptr;   // lo plane follows hi
+                    e = build_flat_level_image(hi, lo, wl, ix->flat_fbase, ix->flat_fshift,
+                                               (uint32_t*)ix->d_flatimg + (1ull << D), st);
+                }
                 if (e != cudaSuccess) return fail_cuda(e, "flat table + level image");
                 ix->flat_img_words = (uint32_t)wl;
             }
@@ -357,7 +371,7 @@ int bs_build(const void* keys, uint64_t n, const bs_layout* layout_in, void** ou
     if (lay.out_bytes == 4 && n >= (1ull << 31)) return fail(BS_ERR_INVALID, "out_bytes = 4 requires n < 2^31");
     if (lay.variant > BS_VARIANT_KARY) return fail(BS_ERR_INVALID, "unknown variant %u", lay.variant);
     if (lay.schedule > BS_SCHED_STATIC) return fail(BS_ERR_INVALID, "unknown schedule %u", lay.schedule);
-    if (lay.reorder > BS_REORDER_SORTED) return fail(BS_ERR_INVALID, "unknown reorder %u", lay.reorder);
+    if (lay.reorder > BS_REORDER_GLOBAL) return fail(BS_ERR_INVALID, "unknown reorder %u", lay.reorder);
     if (lay.kary_mode > BS_KARY_MODE_AUTO) return fail(BS_ERR_INVALID, "unknown kary_mode %u", lay.kary_mode);
     if (lay.k < 2 || lay.k > 33) return fail(BS_ERR_INVALID, "K must be in [2, 33]");
     if (lay.leaf_chunk != 0 && (!is_pow2(lay.leaf_chunk) || lay.leaf_chunk > 256))
@@ -535,7 +549,8 @@ int bs_launch_default(const void* idx, bs_launch* l) {
     return BS_OK;
 }
 
-int bs_lookup_ex(const void* idx, const void* queries, uint64_t m, void* out, void* stream, const bs_launch* launch) {
+static int lookup_impl(const void* idx, const void* queries, uint64_t m, void* out, void* stream,
+                       const bs_launch* launch, void* ws, uint64_t ws_bytes) {
     if (!idx) return fail(BS_ERR_INVALID, "bs_lookup: idx is NULL");
     const Index* ix = (const Index*)idx;
     bs_launch L;
@@ -546,7 +561,7 @@ int bs_lookup_ex(const void* idx, const void* queries, uint64_t m, void* out, vo
         bs_launch_default(idx, &L);
     }
     if (L.kary_mode > 7) return fail(BS_ERR_INVALID, "bs_lookup: unknown kary_mode %u", L.kary_mode);
-    if (L.reorder > BS_REORDER_SORTED) return fail(BS_ERR_INVALID, "bs_lookup: unknown reorder %u", L.reorder);
+    if (L.reorder > BS_REORDER_GLOBAL) return fail(BS_ERR_INVALID, "bs_lookup: unknown reorder %u", L.reorder);
     if (m == 0) return BS_OK;
     if (!queries || !out) return fail(BS_ERR_INVALID, "bs_lookup: NULL queries/out with m > 0");
     const uintptr_t q0 = (uintptr_t)queries, q1 = q0 + m * ix->kb;
@@ -556,7 +571,50 @@ int bs_lookup_ex(const void* idx, const void* queries, uint64_t m, void* out, vo
     if (!device_accessible(queries, ix->device) || !device_accessible(out, ix->device))
         return fail(BS_ERR_INVALID, "bs_lookup: queries/out must be device memory of the index's GPU "
                                     "(host buffers: bs_lookup_host)");
+    if (L.reorder == BS_REORDER_GLOBAL) {
+        uint64_t need = 0;
+        if (!part_workspace_bytes(ix->n, m, ix->kb, ix->ob, &need))
+            return fail(BS_ERR_UNSUPPORTED, "BS_REORDER_GLOBAL: needs n <= 2^27 keys and m < 2^32");
+        if (!ws) return fail(BS_ERR_INVALID, "BS_REORDER_GLOBAL needs a workspace: bs_lookup_ws");
+        if (ws_bytes < need)
+            return fail(BS_ERR_INVALID, "bs_lookup_ws: workspace of %llu B < %llu B", (unsigned long long)ws_bytes,
+                        (unsigned long long)need);
+        if (!device_accessible(ws, ix->device)) return fail(BS_ERR_INVALID, "bs_lookup_ws: ws must be device memory");
+        bool uns = false;
+        cudaError_t e = launch_part_global(ix->kb, ix->ob, ix->d_keys, ix->n, queries, m, out,
+                                           (L.cache_hints & BS_HINT_STREAM_EVICT_FIRST) ? 1u : 0u, ws, ws_bytes,
+                                           (uint32_t)ix->sm_count, (cudaStream_t)stream, &uns);
+        if (uns) return fail(BS_ERR_UNSUPPORTED, "BS_REORDER_GLOBAL: not supported for this index / batch");
+        if (e != cudaSuccess) return fail_cuda(e, "global partition launch");
+        return BS_OK;
+    }
     return dispatch_lookup(ix, queries, m, out, (cudaStream_t)stream, L);
+}
+
+int bs_lookup_ex(const void* idx, const void* queries, uint64_t m, void* out, void* stream, const bs_launch* launch) {
+    return lookup_impl(idx, queries, m, out, stream, launch, nullptr, 0);
+}
+
+int bs_lookup_ws(const void* idx, const void* queries, uint64_t m, void* out, void* stream, const bs_launch* launch,
+                 void* ws, uint64_t ws_bytes) {
+    return lookup_impl(idx, queries, m, out, stream, launch, ws, ws_bytes);
+}
+
+int bs_workspace_bytes(const void* idx, uint64_t m, const bs_launch* launch, uint64_t* bytes) {
+    if (!idx || !bytes) return fail(BS_ERR_INVALID, "bs_workspace_bytes: NULL");
+    const Index* ix = (const Index*)idx;
+    bs_launch L;
+    if (launch) {
+        if (launch->struct_size != sizeof(bs_launch)) return fail(BS_ERR_INVALID, "bs_launch.struct_size mismatch");
+        L = *launch;
+    } else {
+        bs_launch_default(idx, &L);
+    }
+    *bytes = 0;
+    if (L.reorder != BS_REORDER_GLOBAL) return BS_OK;
+    if (!part_workspace_bytes(ix->n, m, ix->kb, ix->ob, bytes))
+        return fail(BS_ERR_UNSUPPORTED, "BS_REORDER_GLOBAL: needs n <= 2^27 keys and m < 2^32");
+    return BS_OK;
 }
 
 int bs_lookup(const void* idx, const void* queries, uint64_t m, void* out, void* stream) {

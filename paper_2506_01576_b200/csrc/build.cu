@@ -174,9 +174,16 @@ cudaError_t build_kary_image(int kb, const void* sep, uint32_t W, uint32_t L, co
 // (span keys per node), the rest are MAX.  Slot 0 is unused.  Probes at depth
 // d touch the contiguous slots [2^d, 2^(d+1)), so lanes spread over banks
 // (a plain sorted array makes every lane of a halving step hit one bank).
+// order-preserving 32-bit image of a u64 key (Index::flat_fbase / flat_fshift)
+__device__ __forceinline__ uint32_t flat_image64(uint64_t x, uint64_t base, uint32_t sh) {
+    if (x <= base) return 0u;
+    const uint64_t d = (x - base) >> sh;
+    return d > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)d;
+}
+
 template <class K>
 __global__ void k_build_flat(const K* __restrict__ a, uint64_t n, uint64_t span, uint64_t M, uint32_t D,
-                             uint32_t* __restrict__ f32, uint64_t* __restrict__ f64) {
+                             uint32_t* __restrict__ f32, uint64_t* __restrict__ f64, uint64_t fbase, uint32_t fshift) {
     const uint64_t slots = 1ull << D;
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < slots;
          k += (uint64_t)gridDim.x * blockDim.x) {
@@ -191,7 +198,7 @@ __global__ void k_build_flat(const K* __restrict__ a, uint64_t n, uint64_t span,
             }
         }
         if constexpr (sizeof(K) == 8) {
-            f32[k] = (uint32_t)((uint64_t)v >> 32);
+            f32[k] = flat_image64((uint64_t)v, fbase, fshift);
             f64[k] = (uint64_t)v;
         } else {
             f32[k] = (uint32_t)v;
@@ -200,14 +207,29 @@ __global__ void k_build_flat(const K* __restrict__ a, uint64_t n, uint64_t span,
 }
 
 cudaError_t build_flat_table(int kb, const void* a, uint64_t n, uint64_t span, uint64_t M, uint32_t D,
-                             void* flat32, void* flat64, cudaStream_t s) {
+                             void* flat32, void* flat64, uint64_t fbase, uint32_t fshift, cudaStream_t s) {
     const uint64_t slots = 1ull << D;
     if (kb == 8)
         k_build_flat<uint64_t><<<grid_for(slots, 256), 256, 0, s>>>((const uint64_t*)a, n, span, M, D,
-                                                                    (uint32_t*)flat32, (uint64_t*)flat64);
+                                                                    (uint32_t*)flat32, (uint64_t*)flat64, fbase, fshift);
     else
         k_build_flat<uint32_t><<<grid_for(slots, 256), 256, 0, s>>>((const uint32_t*)a, n, span, M, D,
-                                                                    (uint32_t*)flat32, nullptr);
+                                                                    (uint32_t*)flat32, nullptr, 0, 0);
+    return cudaGetLastError();
+}
+
+// the flat level's node image in the flat table's 32-bit image (u64: from the
+// hi / lo planes of the tiered image; u32: the plane as is)
+__global__ void k_flat_level_image(const uint32_t* __restrict__ hi, const uint32_t* __restrict__ lo, uint64_t words,
+                                   uint64_t fbase, uint32_t fshift, uint32_t* __restrict__ out) {
+    for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < words; w += (uint64_t)gridDim.x * blockDim.x)
+        out[w] = lo ? flat_image64(((uint64_t)hi[w] << 32) | lo[w], fbase, fshift) : hi[w];
+}
+
+cudaError_t build_flat_level_image(const uint32_t* hi, const uint32_t* lo, uint64_t words, uint64_t fbase,
+                                   uint32_t fshift, uint32_t* out, cudaStream_t s) {
+    if (!words) return cudaSuccess;
+    k_flat_level_image<<<grid_for(words, 256), 256, 0, s>>>(hi, lo, words, fbase, fshift, out);
     return cudaGetLastError();
 }
 

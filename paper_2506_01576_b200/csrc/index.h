@@ -84,6 +84,11 @@ struct Index {
     void* d_flatimg = nullptr;       // [flat table (2^flat_D words) | flat level's node image], one stage
     uint32_t flat_img_words = 0;     // words of the level image (0: not built)
     uint32_t flat_level = 0, flat_D = 0;   // Eytzinger slots 1..2^flat_D - 1
+    // u64: the flat table and its level image hold F(x) = min((x - flat_fbase) >> flat_fshift,
+    // 2^32 - 1) (0 below the base), an order-preserving 32-bit image; flat_fshift makes the
+    // array's span fit 32 bits (the hi word when the keys span 2^64; exact when < 2^32)
+    uint64_t flat_fbase = 0;
+    uint32_t flat_fshift = 32;
 
     // device
     int sm_count = 148, smem_optin = 232448, smem_per_sm = 233472, l2_bytes = 0;

@@ -45,6 +45,62 @@ __device__ __forceinline__ void ld_node(const K* p, bool hint, uint64_t pol, K* 
     }
 }
 
+// Order-preserving 32-bit image of a u64 key for the flat table and its level
+// image (KaryParams::fbase / fshift; the hi word when the keys span 2^64, exact
+// when they span < 2^32, so keys sharing their hi word do not tie).
+__device__ __forceinline__ uint32_t flat_image(uint64_t x, uint64_t base, uint32_t sh) {
+    if (x <= base) return 0u;
+    const uint64_t d = (x - base) >> sh;
+    return d > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)d;
+}
+
+// #{slots < q} of one image node (W sorted 32-bit slots) by binary search; `tie`
+// records a probe equal to q's image (then the count may be short, fixed later)
+template <int W>
+__device__ __forceinline__ uint32_t img32_rank(const uint32_t* S, uint32_t nd, uint32_t fq, bool extra, bool& tie) {
+    uint32_t c = 0;
+#pragma unroll
+    for (int s = W / 2; s >= 1; s >>= 1) {
+        const uint32_t h = S[nd + c + s - 1];
+        tie |= h == fq;
+        c += h < fq ? (uint32_t)s : 0u;
+    }
+    if (extra) {
+        const uint32_t h = S[nd + c];
+        tie |= h == fq;
+        c += h < fq ? 1u : 0u;
+    }
+    return c;
+}
+
+// First node c' >= c whose maximum a[min((c'+1)*span, n) - 1] is >= q, or M:
+// the exact node after a descent over images that only bound it from below.
+// Galloping then bisection: O(log #tied maxima) reads, never a linear walk.
+template <class K>
+__device__ __forceinline__ uint64_t step_over_ties(const K* __restrict__ a, uint64_t n, uint64_t span, uint64_t M,
+                                                   uint64_t c, K q) {
+    auto mx = [&](uint64_t i) -> K {
+        uint64_t e = (i + 1) * span;
+        if (e > n) e = n;
+        return ldg(a + e - 1);
+    };
+    if (c >= M || mx(c) >= q) return c;
+    uint64_t l = c + 1, step = 1, h;
+    for (;;) {
+        h = l - 1 + step;
+        if (h >= M) { h = M; break; }
+        if (mx(h) >= q) break;
+        l = h + 1;
+        step <<= 1;
+    }
+    while (l < h) {
+        const uint64_t mid = l + ((h - l) >> 1);
+        if (mx(mid) < q) l = mid + 1;
+        else h = mid;
+    }
+    return l;
+}
+
 // OBC != 0: the output width is a compile-time constant (the FLAT T = 1
 // instance for out_bytes == key_bytes), so the epilogue carries no width select
 template <class K, int W, int GL, int IL, int T, bool FLAT, bool PEER = false, int OBC = 0>
@@ -145,18 +201,19 @@ k_kary_g1(const KaryParams<K> p, const K* __restrict__ q, uint64_t m_arg, void* 
             const uint32_t D = p.flat_D;
             const uint32_t sb = smem_u32(S);
             const uint32_t step_lt = 4u - sb, step_ge = 0u - sb;
-            uint32_t a[T], k[T];
+            uint32_t a[T], k[T], fq[T];
 #pragma unroll
-            for (int t = 0; t < T; ++t) a[t] = sb + 4u;
+            for (int t = 0; t < T; ++t) {
+                a[t] = sb + 4u;
+                if constexpr (sizeof(K) == 8) fq[t] = flat_image((uint64_t)key[t], p.fbase, p.fshift);
+                else fq[t] = (uint32_t)key[t];
+            }
 #pragma unroll 4
             for (uint32_t d = 0; d < D; ++d) {
 #pragma unroll
                 for (int t = 0; t < T; ++t) {
                     const uint32_t h = lds_u32(a[t]);
-                    bool less;
-                    if constexpr (sizeof(K) == 8) less = h < (uint32_t)((uint64_t)key[t] >> 32);
-                    else less = h < (uint32_t)key[t];
-                    a[t] = 2u * a[t] + (less ? step_lt : step_ge);
+                    a[t] = 2u * a[t] + (h < fq[t] ? step_lt : step_ge);
                 }
             }
 #pragma unroll
@@ -165,7 +222,7 @@ k_kary_g1(const KaryParams<K> p, const K* __restrict__ q, uint64_t m_arg, void* 
                 node[t] = k[t] - (1u << D);
                 if constexpr (sizeof(K) == 8) {
                     const uint32_t j = k[t] >> __ffs(~k[t]);
-                    tie |= j != 0 && S[j] == (uint32_t)((uint64_t)key[t] >> 32);
+                    tie |= j != 0 && S[j] == fq[t];
                 }
             }
             if (p.flat_img_words) {
@@ -173,30 +230,20 @@ k_kary_g1(const KaryParams<K> p, const K* __restrict__ q, uint64_t m_arg, void* 
                 const uint32_t last = p.nodes_next[Ls - 1] - 1;
 #pragma unroll
                 for (int t = 0; t < T; ++t) {
-                    const uint32_t c = smem_node_rank<K, W, false, false>(S, (1u << D) + node[t] * (W + 1), key[t],
-                                                                          extra, tie);
+                    const uint32_t c = img32_rank<W>(S, (1u << D) + node[t] * (W + 1), fq[t], extra, tie);
                     const uint32_t child = node[t] * K_ + c;
                     node[t] = child < last ? child : last;
                 }
             }
             if constexpr (sizeof(K) == 8) {
-                // hi-word ties: node = #(maxima whose hi word < q's), a lower
-                // bound on the exact count; the tied lanes step over the maxima
-                // that share q's hi word and are still < q — read straight from
-                // the sorted array (max of node c = a[min((c+1)*span, n) - 1]),
-                // usually one load instead of redoing all D levels
+                // image ties: node = #(maxima whose image < q's), a lower bound on
+                // the exact count; the tied lanes step over the maxima that are
+                // still < q — read from the sorted array (max of node c =
+                // a[min((c+1)*span, n) - 1]), galloping: usually one read
                 if (__any_sync(0xFFFFFFFFu, tie) && tie) {
 #pragma unroll 1
-                    for (int t = 0; t < T; ++t) {
-                        uint64_t c = node[t];
-                        while (c < p.flat_M) {
-                            uint64_t end = (c + 1) * p.flat_span;
-                            if (end > n) end = n;
-                            if (ldg(p.a + end - 1) < (uint64_t)key[t]) ++c;
-                            else break;
-                        }
-                        node[t] = (uint32_t)c;
-                    }
+                    for (int t = 0; t < T; ++t)
+                        node[t] = (uint32_t)step_over_ties(p.a, n, p.flat_span, p.flat_M, node[t], key[t]);
                 }
             }
         } else {
@@ -219,16 +266,8 @@ k_kary_g1(const KaryParams<K> p, const K* __restrict__ q, uint64_t m_arg, void* 
             // read from the sorted array — usually one load)
             if (__any_sync(0xFFFFFFFFu, tie) && tie) {
 #pragma unroll 1
-                for (int t = 0; t < T; ++t) {
-                    uint64_t c = node[t];
-                    while (c < p.flat_M) {
-                        uint64_t end = (c + 1) * p.flat_span;
-                        if (end > n) end = n;
-                        if (ldg(p.a + end - 1) < (uint64_t)key[t]) ++c;
-                        else break;
-                    }
-                    node[t] = (uint32_t)c;
-                }
+                for (int t = 0; t < T; ++t)
+                    node[t] = (uint32_t)step_over_ties(p.a, n, p.flat_span, p.flat_M, node[t], key[t]);
             }
         }
         }
@@ -360,7 +399,7 @@ k_kary_g1p(const KaryParams<K> p, const K* __restrict__ q, uint64_t m, void* __r
         const uint32_t h = S[k];
         bool less;
         if constexpr (sizeof(K) == 8) {
-            const uint32_t qh = (uint32_t)((uint64_t)kq >> 32);
+            const uint32_t qh = flat_image((uint64_t)kq, p.fbase, p.fshift);
             less = h < qh;
             tie |= h == qh;
         } else {

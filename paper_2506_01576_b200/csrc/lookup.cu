@@ -209,6 +209,8 @@ static int run_kary(const Index* ix, const void* q, uint64_t m, void* out, cudaS
             p.flat_D = ix->flat_D;
             p.flat_M = ix->flat_M;
             p.flat_span = ix->flat_span;
+            p.fbase = ix->flat_fbase;
+            p.fshift = ix->flat_fshift;
             p.smem_bytes = (4u << ix->flat_D) + 16;
             p.flat_img_words = 0;
             const uint64_t with_img = ((1ull << ix->flat_D) + ix->flat_img_words) * 4 + 16;

@@ -61,6 +61,8 @@ struct KaryParams {
     uint64_t flat_M;         // node maxima in the table (sorted position c < flat_M)
     uint64_t flat_span;      // keys under one node of level Ls: max of node c = a[min((c+1)*span, n) - 1]
     uint32_t flat_img_words; // > 0: the flat level's node image follows the table in smem (mode 7 descends it)
+    uint64_t fbase;          // u64 flat image: F(x) = min((x - fbase) >> fshift, 2^32 - 1), 0 below fbase
+    uint32_t fshift;
     // fused peer-memory routing (peer.cu, bs_lookup_peer; g1 kernels only).
     // peer_cursor == nullptr: a plain lookup.  Otherwise the kernel first waits
     // until *peer_wait >= peer_wait_target (every rank has routed its queries
@@ -108,6 +110,11 @@ struct Grid { uint32_t sched_static, ctas_per_sm, sm_count; };
 
 cudaError_t launch_seg_sorted(int kb, int ob, const void* a, uint64_t n, const void* q, uint64_t m, void* out,
                               uint32_t stream_hint, Grid grid, cudaStream_t s, bool* uns);
+// BS_REORDER_GLOBAL (seg.cu): partition -> segment lookups -> unpartition in a caller workspace
+bool part_workspace_bytes(uint64_t n, uint64_t m, int kb, int ob, uint64_t* bytes);
+cudaError_t launch_part_global(int kb, int ob, const void* a, uint64_t n, const void* q, uint64_t m, void* out,
+                               uint32_t stream_hint, void* ws, uint64_t ws_bytes, uint32_t sm_count, cudaStream_t s,
+                               bool* uns);
 
 // Shared-memory carve-out of a kernel (cudaFuncAttributePreferredSharedMemoryCarveout,
 // percent of the SM's 228 KB unified L1/shared array): the smallest that holds the
@@ -172,7 +179,9 @@ cudaError_t build_kary_image(int kb, const void* sep, uint32_t W, uint32_t L, co
                               const uint64_t* lvl_nodes, const uint32_t* img_base, uint64_t plane_words,
                               void* img, bool pair64, cudaStream_t s);
 cudaError_t build_flat_table(int kb, const void* a, uint64_t n, uint64_t span, uint64_t M, uint32_t D,
-                             void* flat32, void* flat64, cudaStream_t s);
+                             void* flat32, void* flat64, uint64_t fbase, uint32_t fshift, cudaStream_t s);
+cudaError_t build_flat_level_image(const uint32_t* hi, const uint32_t* lo, uint64_t words, uint64_t fbase,
+                                   uint32_t fshift, uint32_t* out, cudaStream_t s);
 cudaError_t build_sort_keys(int kb, const void* in, void* out, uint64_t n, cudaStream_t s);
 
 // ---- multi-GPU routing kernels (dist.cu) ----

@@ -258,3 +258,24 @@ def test_info_footprint():
     assert info["separator_bytes"] >= 32800 * 4
     assert info["footprint_bytes"] >= info["array_bytes"] + info["separator_bytes"]
     assert info["build_ms"] > 0
+
+
+# ------------------------------------------------------------------ u64 keys in a narrow range (hi-word ties)
+
+@pytest.mark.parametrize("hi_log2", [20, 32, 40, 48])
+def test_u64_narrow_key_range(hi_log2):
+    """u64 keys confined to [0, 2^hi): with the high word alone every probe of the
+    flat table would tie; the order-preserving image (span in 32 bits) and the
+    galloping fix-up must give the oracle's results for every schedule."""
+    from workload import device as wd
+    n = min(1 << 20, (1 << hi_log2) // 4)
+    keys = wd.gen_keys_range(n, 0, 1 << hi_log2, 77, 0, device="cpu").numpy().view(np.uint64)
+    q = np.concatenate([workload.gen_queries(keys, 200000, seed=3, hit_ratio=0.8),
+                        workload.adversarial_queries(keys[::97], seed=5, extra=500)])
+    want = oracle.lookup(keys, q)
+    idx = build(keys, variant=bs.KARY)
+    check(run(idx, q, 8), want, q, f"default hi={hi_log2}")
+    for mode in (6, 7):
+        check(run(idx, q, 8, kary_mode=mode), want, q, f"mode {mode} hi={hi_log2}")
+    check(run(idx, q, 8, kary_mode=7, nreg=0x34), want, q, f"pipelined hi={hi_log2}")
+    idx.close()
