@@ -616,7 +616,7 @@ def main():
     bpl, bpl_why = algorithmic_bytes_per_lookup(cfg, kb, ob, args.order, n_loc, m, l2_bytes)
     achieved = bpl * m / (ms_step / 1e3) / 1e9          # per GPU (max-over-ranks time)
     tkey = (f"{cfg}/{args.order}/{args.variant}/K{info['k']}/C{info['leaf_chunk']}/mode{launch.kary_mode}"
-            + ("/peer" if mode == "partitioned" else ""))
+            + ("/peer" if mode == "partitioned" else "") + (f"/r{launch.reorder}" if launch.reorder else ""))
     te = traffic_entry(tkey)
     traffic = None
     if te and te.get("queries") == m:
@@ -627,8 +627,11 @@ def main():
             "traffic_frac": traffic / (ms_step / 1e3) / 1e9 / peak if traffic else None,
             "traffic_key": tkey, "alg_bytes_per_launch": bpl * m, "bytes_per_lookup_alg": bpl,
             "bytes_per_lookup_model": bpl_why, "peak_source": peak_src, "per": "GPU"}
-    if te and te.get("l2"):
-        roof["l2"] = te["l2"]
+    if te and te.get("kernels"):
+        # a step of several kernels: the roofline is the step's (sum of its launches); shares beside it
+        roof["kernels"] = [{"kernel": k["kernel"], "share_ncu": k["ms"] / te["ncu_ms"],
+                            "dram_B_per_lookup": k["dram_B_per_lookup"]} for k in te["kernels"]]
+        roof["traffic_per_lookup"] = te["dram_bytes_per_lookup"]
 
     line = {
         "metric": METRIC, "value": value, "unit": "lookups/s", "n_gpus": world, "steps": args.steps,

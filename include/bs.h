@@ -70,7 +70,7 @@ typedef enum {
                               point): one partition pass groups the queries by the
                               8192-key segment that holds their answer (records in a caller
                               workspace), the segment-staged lookup runs per segment, one pass
-                              restores query order.  Needs bs_lookup_ws; n <= 2^27 keys.     */
+                              restores query order.  Needs bs_lookup_ws; n <= 2^26 keys.     */
 } bs_reorder;
 
 /* Build-time structure + default launch configuration.
@@ -165,11 +165,14 @@ typedef struct {
     uint32_t kary_smem_levels;   /* top K-ary levels staged in shared memory              */
     uint64_t separator_slots;    /* K-ary slots incl. padding (node_slots per node)       */
     uint64_t separator_bytes;
-    double build_ms;             /* device time of bs_build (Fig. 13)               */
+    double build_ms;             /* device time from bs_build's first to last stream op (incl. gaps) */
     uint32_t sm_count;
     uint32_t smem_per_cta_opt;   /* dynamic shared memory of the OPT kernel (bytes)       */
     uint32_t smem_per_cta_kary;
-    uint32_t reserved[5];
+    uint32_t build_stage_us[5];  /* device time of each build stage in microseconds, allocation
+                                    excluded (Fig. 13): [0] radix sort of unsorted
+                                    input, [1] sortedness check of sorted input, [2] pinned table,
+                                    [3] K-ary separators, [4] shared-memory images + flat table */
 } bs_info;
 
 /* Debug exports (layout-fidelity tests) for bs_export(). */
@@ -253,7 +256,7 @@ int bs_lookup_host(const void* idx, const void* host_queries, uint64_t m, void* 
  *   bs_workspace_bytes: *bytes = device bytes a bs_lookup_ws call with this
  *     launch (NULL = index defaults) needs for m queries (0 if the mode needs
  *     none).  BS_ERR_UNSUPPORTED if the mode cannot run on this index (GLOBAL:
- *     n > 2^27 keys, or m >= 2^32).
+ *     n > 2^26 keys, or m >= 2^32).
  *   bs_lookup_ws: bs_lookup_ex plus a caller-owned device workspace `ws` of
  *     ws_bytes (no allocation inside; the workspace must not be shared by calls
  *     in flight on other streams).  BS_ERR_INVALID if ws is NULL / too small for

@@ -54,10 +54,12 @@ class bs_info(ctypes.Structure):
                 ("kary_levels", _u32), ("k", _u32), ("leaf_chunk", _u32), ("node_slots", _u32),
                 ("kary_smem_levels", _u32), ("separator_slots", _u64), ("separator_bytes", _u64),
                 ("build_ms", ctypes.c_double), ("sm_count", _u32), ("smem_per_cta_opt", _u32),
-                ("smem_per_cta_kary", _u32), ("reserved", _u32 * 5)]
+                ("smem_per_cta_kary", _u32), ("build_stage_us", _u32 * 5)]
 
     def as_dict(self):
-        return {f: (getattr(self, f) if f != "reserved" else None) for f, _ in self._fields_ if f != "reserved"}
+        d = {f: getattr(self, f) for f, _ in self._fields_ if f != "build_stage_us"}
+        d["build_stage_us"] = list(self.build_stage_us)
+        return d
 
 
 class BsError(RuntimeError):

@@ -171,9 +171,48 @@ void table_prefix(const Index* ix, uint64_t entries, bool partial, uint32_t* D, 
     *P = (uint32_t)p;
 }
 
+// Device time of each build stage (bs_info.build_stage_us): an event pair
+// brackets every group of build kernels, so cudaMalloc and host work between
+// them are not counted (Fig. 13).
+enum BuildStage { kStSort = 0, kStCheck = 1, kStTable = 2, kStSep = 3, kStImg = 4, kStages = 5 };
+struct BuildTimer {
+    static constexpr int kMax = 24;
+    cudaEvent_t a[kMax] = {}, b[kMax] = {};
+    int stage[kMax] = {};
+    int used = 0, open = -1;
+    cudaStream_t st = nullptr;
+    void begin(int s) {
+        if (used >= kMax) return;
+        if (!a[used]) { cudaEventCreate(&a[used]); cudaEventCreate(&b[used]); }
+        stage[used] = s;
+        cudaEventRecord(a[used], st);
+        open = used;
+    }
+    void end() {
+        if (open < 0) return;
+        cudaEventRecord(b[open], st);
+        ++used;
+        open = -1;
+    }
+    void collect(float* ms) {   // after a stream sync
+        for (int i = 0; i < kStages; ++i) ms[i] = 0;
+        for (int i = 0; i < used; ++i) {
+            float t = 0;
+            if (cudaEventElapsedTime(&t, a[i], b[i]) == cudaSuccess) ms[stage[i]] += t;
+        }
+        cudaGetLastError();
+    }
+    ~BuildTimer() {
+        for (int i = 0; i < kMax; ++i) {
+            if (a[i]) cudaEventDestroy(a[i]);
+            if (b[i]) cudaEventDestroy(b[i]);
+        }
+    }
+};
+
 static uint64_t chunks_of(const Index* ix) { return (ix->n + ix->kC - 1) / ix->kC; }
 
-static int build_kary_layout(Index* ix, cudaStream_t st) {
+static int build_kary_layout(Index* ix, cudaStream_t st, BuildTimer& bt) {
     const uint64_t n = ix->n;
     const uint32_t K = ix->kK, C = ix->kC, W = ix->kW;
     // bottom-up node counts, then reverse to top-first
@@ -206,7 +245,9 @@ static int build_kary_layout(Index* ix, cudaStream_t st) {
     if (e != cudaSuccess) return fail_cuda(e, "cudaMalloc(separators)");
     e = cudaMemsetAsync(ix->d_sep, 0xFF, bytes, st);
     if (e != cudaSuccess) return fail_cuda(e, "memset(separators)");
+    bt.begin(kStSep);
     e = build_kary_levels(kb, ix->d_keys, n, K, C, W, L, ix->k_base, ix->k_nodes, ix->d_sep, slot, st);
+    bt.end();
     if (e != cudaSuccess) return fail_cuda(e, "build_kary_levels");
     // tiered shared-memory image: the longest level prefix whose planes fit one CTA's shared memory
     {
@@ -230,7 +271,9 @@ static int build_kary_layout(Index* ix, cudaStream_t st) {
             if (e != cudaSuccess) return fail_cuda(e, "cudaMalloc(shared image)");
             uint64_t nodes[kMaxKaryLevels];
             for (uint32_t l = 0; l < Li; ++l) nodes[l] = ix->k_nodes[l];
+            bt.begin(kStImg);
             e = build_kary_image(kb, ix->d_sep, W, Li, ix->k_base, nodes, ix->img_base, words, ix->d_img, false, st);
+            bt.end();
             if (e != cudaSuccess) return fail_cuda(e, "build_kary_image");
         }
     }
@@ -251,7 +294,9 @@ static int build_kary_layout(Index* ix, cudaStream_t st) {
             if (e != cudaSuccess) return fail_cuda(e, "cudaMalloc(shared image 64)");
             uint64_t nodes[kMaxKaryLevels];
             for (uint32_t l = 0; l < Li; ++l) nodes[l] = ix->k_nodes[l];
+            bt.begin(kStImg);
             e = build_kary_image(kb, ix->d_sep, W, Li, ix->k_base, nodes, ix->img64_base, slots, ix->d_img64, true, st);
+            bt.end();
             if (e != cudaSuccess) return fail_cuda(e, "build_kary_image(64)");
         }
     }
@@ -291,8 +336,10 @@ static int build_kary_layout(Index* ix, cudaStream_t st) {
             ix->flat_fbase = ix->a_first;
             ix->flat_fshift = bl > 32 ? bl - 32 : 0;
         }
+        bt.begin(kStImg);
         e = build_flat_table(kb, ix->d_keys, n, span, ix->flat_M, D, ix->d_flat, ix->d_flat64, ix->flat_fbase,
                              ix->flat_fshift, st);
+        bt.end();
         if (e != cudaSuccess) return fail_cuda(e, "build_flat_table");
         // the flat level's node image next to the table (one buffer, one TMA
         // stage): mode 7 then descends one shared level below the table
@@ -306,8 +353,10 @@ static int build_kary_layout(Index* ix, cudaStream_t st) {
                 if (e == cudaSuccess) {
                     const uint32_t* hi = (const uint32_t*)ix->d_img + ix->img_base[lt];
                     const uint32_t* lo = kb == 8 ? hi + ix->img_base[ix->img_L] : nullptr;   // lo plane follows hi
+                    bt.begin(kStImg);
                     e = build_flat_level_image(hi, lo, wl, ix->flat_fbase, ix->flat_fshift,
                                                (uint32_t*)ix->d_flatimg + (1ull << D), st);
+                    bt.end();
                 }
                 if (e != cudaSuccess) return fail_cuda(e, "flat table + level image");
                 ix->flat_img_words = (uint32_t)wl;
@@ -394,6 +443,7 @@ int bs_build(const void* keys, uint64_t n, const bs_layout* layout_in, void** ou
     cudaError_t e;
     cudaStream_t st = nullptr;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
+    BuildTimer bt;
     int* d_flag = nullptr;
     const size_t abytes = n * ix->kb;
 
@@ -421,6 +471,7 @@ int bs_build(const void* keys, uint64_t n, const bs_layout* layout_in, void** ou
     }
     e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
     if (e != cudaSuccess) { rc = fail_cuda(e, "cudaStreamCreate"); goto done; }
+    bt.st = st;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventRecord(e0, st);
@@ -446,7 +497,9 @@ int bs_build(const void* keys, uint64_t n, const bs_layout* layout_in, void** ou
             e = cudaMallocAsync((void**)&d_flag, sizeof(int), st);
             if (e != cudaSuccess) { rc = fail_cuda(e, "cudaMalloc(flag)"); goto done; }
             cudaMemsetAsync(d_flag, 0, sizeof(int), st);
+            bt.begin(kStCheck);
             e = build_check_sorted(ix->kb, ix->d_keys, n, d_flag, st);
+            bt.end();
             if (e != cudaSuccess) { rc = fail_cuda(e, "check_sorted"); goto done; }
             int flag = 0;
             cudaMemcpyAsync(&flag, d_flag, sizeof(int), cudaMemcpyDeviceToHost, st);
@@ -458,7 +511,9 @@ int bs_build(const void* keys, uint64_t n, const bs_layout* layout_in, void** ou
             e = cudaMallocAsync(&tmp, abytes, st);
             if (e != cudaSuccess) { rc = fail_cuda(e, "cudaMalloc(sort tmp)"); goto done; }
             e = cudaMemcpyAsync(tmp, keys, abytes, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st);
+            bt.begin(kStSort);
             if (e == cudaSuccess) e = build_sort_keys(ix->kb, tmp, ix->d_keys, n, st);
+            bt.end();
             cudaFreeAsync(tmp, st);
             if (e != cudaSuccess) { rc = fail_cuda(e, "radix sort"); goto done; }
         }
@@ -481,7 +536,9 @@ int bs_build(const void* keys, uint64_t n, const bs_layout* layout_in, void** ou
             if (e != cudaSuccess) { rc = fail_cuda(e, "cudaMalloc(table)"); goto done; }
             uint32_t bases[kMaxLevels + 1];
             for (uint32_t d = 0; d <= ix->levels; ++d) bases[d] = (uint32_t)(ix->base_all[d] < 0xFFFFFFFFull ? ix->base_all[d] : 0xFFFFFFFFu);
+            bt.begin(kStTable);
             e = build_pinned_table(ix->kb, ix->d_keys, n, ix->s0, ix->levels, bases, ix->d_tab, entries, st);
+            bt.end();
             if (e != cudaSuccess) { rc = fail_cuda(e, "build_pinned_table"); goto done; }
         }
     }
@@ -505,7 +562,7 @@ int bs_build(const void* keys, uint64_t n, const bs_layout* layout_in, void** ou
     ix->kW = pow2_at_least(lay.k - 1 < 2 ? 2 : lay.k - 1);
     if (ix->kW > 32) { rc = fail(BS_ERR_INVALID, "K - 1 must be <= 32"); goto done; }
     if (lay.variant == BS_VARIANT_KARY) {
-        rc = build_kary_layout(ix, st);
+        rc = build_kary_layout(ix, st, bt);
         if (rc != BS_OK) goto done;
         ix->kary_built = true;
     }
@@ -517,6 +574,7 @@ int bs_build(const void* keys, uint64_t n, const bs_layout* layout_in, void** ou
         float ms = 0;
         cudaEventElapsedTime(&ms, e0, e1);
         ix->build_ms = ms;
+        bt.collect(ix->build_stage_ms);
     }
 
 done:
@@ -573,8 +631,8 @@ static int lookup_impl(const void* idx, const void* queries, uint64_t m, void* o
                                     "(host buffers: bs_lookup_host)");
     if (L.reorder == BS_REORDER_GLOBAL) {
         uint64_t need = 0;
-        if (!part_workspace_bytes(ix->n, m, ix->kb, ix->ob, &need))
-            return fail(BS_ERR_UNSUPPORTED, "BS_REORDER_GLOBAL: needs n <= 2^27 keys and m < 2^32");
+        if (!part_workspace_bytes(ix->n, m, ix->kb, ix->ob, (uint32_t)ix->sm_count, &need))
+            return fail(BS_ERR_UNSUPPORTED, "BS_REORDER_GLOBAL: needs n <= 2^26 keys and m < 2^32");
         if (!ws) return fail(BS_ERR_INVALID, "BS_REORDER_GLOBAL needs a workspace: bs_lookup_ws");
         if (ws_bytes < need)
             return fail(BS_ERR_INVALID, "bs_lookup_ws: workspace of %llu B < %llu B", (unsigned long long)ws_bytes,
@@ -612,8 +670,8 @@ int bs_workspace_bytes(const void* idx, uint64_t m, const bs_launch* launch, uin
     }
     *bytes = 0;
     if (L.reorder != BS_REORDER_GLOBAL) return BS_OK;
-    if (!part_workspace_bytes(ix->n, m, ix->kb, ix->ob, bytes))
-        return fail(BS_ERR_UNSUPPORTED, "BS_REORDER_GLOBAL: needs n <= 2^27 keys and m < 2^32");
+    if (!part_workspace_bytes(ix->n, m, ix->kb, ix->ob, (uint32_t)ix->sm_count, bytes))
+        return fail(BS_ERR_UNSUPPORTED, "BS_REORDER_GLOBAL: needs n <= 2^26 keys and m < 2^32");
     return BS_OK;
 }
 
@@ -650,6 +708,7 @@ int bs_index_info(const void* idx, bs_info* info) {
     if (ix->d_flat) info->footprint_bytes += (1ull << ix->flat_D) * (ix->d_flat64 ? 12 : 4);
     if (ix->d_flatimg) info->footprint_bytes += ((1ull << ix->flat_D) + ix->flat_img_words) * 4;
     info->build_ms = ix->build_ms;
+    for (int i = 0; i < 5; ++i) info->build_stage_us[i] = (uint32_t)(ix->build_stage_ms[i] * 1000.0f + 0.5f);
     info->sm_count = ix->sm_count;
     info->smem_per_cta_opt = (uint32_t)ix->last_opt_smem;
     info->smem_per_cta_kary = (uint32_t)ix->last_kary_smem;

@@ -93,6 +93,7 @@ struct Index {
     // device
     int sm_count = 148, smem_optin = 232448, smem_per_sm = 233472, l2_bytes = 0;
     double build_ms = 0;
+    float build_stage_ms[5] = {};   // sort, sortedness check, pinned table, separators, images + flat table
     // shared memory of the last OPT / K-ary launch (bs_info; atomics: lookups may run concurrently)
     mutable std::atomic<uint64_t> last_opt_smem{0}, last_kary_smem{0};
 

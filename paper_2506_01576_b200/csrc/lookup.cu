@@ -1,5 +1,6 @@
 // lookup.cu — per-call variant dispatch: builds the kernel parameter blocks
 // from the index and the launch knobs, sizes shared memory, launches.
+#include <cstdlib>
 #include <cstring>
 
 #include "index.h"
@@ -161,12 +162,18 @@ static int run_kary(const Index* ix, const void* q, uint64_t m, void* out, cudaS
     p.leaf_hint = (L.cache_hints & BS_HINT_LEAF_EVICT_FIRST) ? 1 : 0;
     p.sep_hint = (L.cache_hints & BS_HINT_SEP_EVICT_LAST) ? 1 : 0;
     {   // separator levels (top-first) whose cumulative bytes fit half the L2 keep evict_last
+        // (BS_SEP_L2_FRAC: A/B knob for the fraction, not part of the ABI)
+        static const double frac = [] {
+            const char* v = getenv("BS_SEP_L2_FRAC");
+            const double f = v ? atof(v) : 0.5;
+            return f > 0.0 && f <= 1.0 ? f : 0.5;
+        }();
         const uint64_t l2 = ix->l2_bytes ? (uint64_t)ix->l2_bytes : (126ull << 20);
         uint64_t cum = 0;
         uint32_t end = 0;
         while (end < ix->kL) {
             const uint64_t lb = ix->k_nodes[end] * ix->kW * ix->kb;
-            if (cum + lb > l2 / 2) break;
+            if (cum + lb > (uint64_t)(l2 * frac)) break;
             cum += lb;
             ++end;
         }

@@ -111,7 +111,7 @@ struct Grid { uint32_t sched_static, ctas_per_sm, sm_count; };
 cudaError_t launch_seg_sorted(int kb, int ob, const void* a, uint64_t n, const void* q, uint64_t m, void* out,
                               uint32_t stream_hint, Grid grid, cudaStream_t s, bool* uns);
 // BS_REORDER_GLOBAL (seg.cu): partition -> segment lookups -> unpartition in a caller workspace
-bool part_workspace_bytes(uint64_t n, uint64_t m, int kb, int ob, uint64_t* bytes);
+bool part_workspace_bytes(uint64_t n, uint64_t m, int kb, int ob, uint32_t sm_count, uint64_t* bytes);
 cudaError_t launch_part_global(int kb, int ob, const void* a, uint64_t n, const void* q, uint64_t m, void* out,
                                uint32_t stream_hint, void* ws, uint64_t ws_bytes, uint32_t sm_count, cudaStream_t s,
                                bool* uns);

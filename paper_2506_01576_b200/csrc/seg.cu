@@ -208,44 +208,44 @@ k_seg_sorted(const SegParams<K> p) {
 
 // ---------------------------------------------------------------- GLOBAL mode
 
-constexpr int kSegLog2 = 13;           // S = 8192 keys per segment: a 32-KB image
-constexpr uint32_t kPartTile = 8192;   // queries per partition tile (slot2 is u16)
-constexpr uint32_t kPartLog2SB = 13;   // at most 2^13 bucket groups in a tile's counting sort
-constexpr uint32_t kPartMaxLog2B = 14; // buckets <= 2^14: the maxima image fits shared memory (64 KB)
+constexpr int kSegLog2 = 13;           // SORTED: S = 8192 keys per segment (a 32-KB image)
+constexpr int kGlobLog2 = 15;          // GLOBAL: S = 32768 keys per bucket segment (a 128-KB image)
+constexpr uint32_t kPartTile = 8192;   // queries per partition tile (u16 positions)
+constexpr uint32_t kGlobMaxB = 2048;   // buckets (n <= 2^26 keys): per-bucket counters fit shared memory
 
-template <class K> struct PartRec;
-template <> struct __align__(16) PartRec<uint64_t> { uint64_t q; uint32_t dst; uint32_t pad; };
-template <> struct PartRec<uint32_t> { uint32_t q; uint32_t dst; };
-
+// Slab layout: bucket b's region holds one slab of `cap` queries per partition
+// CTA c (slab(b, c) = (b * G + c) * cap), filled in tile order by that CTA
+// alone — no global atomics, and each CTA keeps only one partly written line
+// per bucket open in L2 (B x G lines, 39 MB at config 3).
 template <class K>
 struct PartParams {
     const K* a;
     uint64_t n, m;
     const K* q;
     void* out;
-    uint64_t B;               // segments
+    uint32_t B;               // buckets (segments of 2^kGlobLog2 keys)
     uint32_t DB;              // log2 of the maxima tree size (2^DB >= B)
-    uint32_t sbsh;            // bucket -> bucket group shift (tile counting sort)
-    uint64_t cap;             // records per bucket region
-    uint32_t* cursor;         // [B] reservations
-    uint32_t* ovf_n;          // overflowed records
-    PartRec<K>* rec;          // [B * cap]
-    PartRec<K>* ovf;          // [m]
-    void* res2;               // [m] results in each tile's bucket-grouped order
-    uint16_t* slot2;          // [m] tile slot of each res2 entry
+    uint32_t G;               // partition CTAs (tile t belongs to CTA t % G)
+    uint32_t cap;             // queries per slab (<= 65535)
+    K* rec;                   // [B * G * cap] queries, bucket-major, slab per CTA
+    void* res;                // [B * G * cap] their results (same positions)
+    uint16_t* slot2;          // [m] tile slot of the tile's j-th query in bucket order
+    uint16_t* b2;             // [m] its bucket
+    uint16_t* thist;          // [ntiles * B] queries of bucket b in tile t
+    uint16_t* tstart;         // [ntiles * B] position of tile t's run in slab(b, t % G)
+    uint32_t* slabcnt;        // [G * B] queries stored per slab
+    uint32_t* ovf_n;          // overflowed queries (slab full: a skewed batch)
+    K* ovf_q;                 // [m]
+    uint32_t* ovf_j;          // [m] their tile-sorted position t * T + j
+    void* res_full;           // [m] results of overflowed queries at t * T + j
     uint32_t stream_hint;
 };
 
-// bucket of x: #(segment maxima < x), maxima max_c = a[(c+1)*S - 1], c < B-1
+// exact bucket from the image bound c: step over maxima still < x (galloping;
+// only when the successor's image ties q's — max_c = a[(c+1)*S - 1], c < B-1)
 template <class K, int D>
-__device__ __forceinline__ uint32_t part_bucket(const uint32_t* MF, uint32_t DB, const K* __restrict__ a, uint64_t B,
-                                                K gbase, uint32_t gsh, K x) {
+__device__ __forceinline__ uint32_t bucket_fix(const K* __restrict__ a, uint32_t nm, uint32_t c, K x) {
     constexpr uint64_t S = 1ull << D;
-    const uint32_t fx = seg_image(x, gbase, gsh);
-    uint32_t k = 1;
-    for (uint32_t d = 0; d < DB; ++d) k = 2u * k + (MF[k] < fx ? 1u : 0u);
-    uint32_t c = k - (1u << DB);              // maxima whose image is below q's: <= bucket
-    const uint32_t nm = (uint32_t)(B - 1);   // maxima in the table
     if (c < nm && ldg(a + ((uint64_t)c + 1) * S - 1) < x) {
         uint32_t l = c + 1, step = 1, h;
         for (;;) {
@@ -265,7 +265,7 @@ __device__ __forceinline__ uint32_t part_bucket(const uint32_t* MF, uint32_t DB,
     return c;
 }
 
-// block-wide exclusive scan of cnt[0..N) in place (blockDim.x = 1024)
+// block-wide exclusive scan of cnt[0..N) in place (blockDim.x a multiple of 32, <= 1024)
 __device__ __forceinline__ void block_exscan(uint32_t* cnt, uint32_t N, uint32_t* warp_tmp) {
     const uint32_t per = (N + blockDim.x - 1) / blockDim.x;
     const uint32_t b0 = threadIdx.x * per;
@@ -282,7 +282,7 @@ __device__ __forceinline__ void block_exscan(uint32_t* cnt, uint32_t N, uint32_t
     if (lane == 31) warp_tmp[w] = inc;
     __syncthreads();
     if (w == 0) {
-        const uint32_t v = lane < (blockDim.x >> 5) ? warp_tmp[lane] : 0u;
+        const uint32_t v = lane < (blockDim.x >> 5) ? warp_tmp[lane] : 0u;   // any blockDim <= 1024
         uint32_t wi = v;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -303,19 +303,24 @@ __device__ __forceinline__ void block_exscan(uint32_t* cnt, uint32_t N, uint32_t
     __syncthreads();
 }
 
+// Partition: per tile of T queries (tile t on CTA t % G), bucket each query, sort
+// the tile by bucket in shared memory, write the tile's (slot, bucket) lists in
+// that order, and append each bucket's run to the CTA's slab of that bucket.
 template <class K, int D>
 __global__ void __launch_bounds__(1024, 1)
 k_part(const PartParams<K> p) {
-    constexpr uint32_t E = kPartTile / 1024;   // queries per thread per tile
+    constexpr uint32_t T = kPartTile, E = T / 1024;
     extern __shared__ __align__(16) uint32_t sm[];
-    const uint32_t DB = p.DB, NT = 1u << DB;
-    const uint32_t NSB = (uint32_t)((p.B - 1) >> p.sbsh) + 1;
-    const bool exact_groups = p.sbsh == 0;      // bucket groups are buckets: one reservation per (tile, bucket)
-    uint32_t* MF = sm;                          // [NT] maxima image (Eytzinger, slot 0 unused)
-    uint32_t* cnt = MF + NT;                    // [NSB] counts, then running ranks
-    uint32_t* off = cnt + NSB;                  // [NSB] tile offsets of the groups
-    uint32_t* gb = off + NSB;                   // [NSB] reserved base in the bucket region (exact groups)
-    uint32_t* warp_tmp = gb + NSB;              // [32]
+    const uint32_t B = p.B, DB = p.DB, NT = 1u << DB;
+    K* stq = reinterpret_cast<K*>(sm);                 // [T] queries in bucket order
+    uint32_t* MF = reinterpret_cast<uint32_t*>(stq + T);   // [NT] maxima image (Eytzinger)
+    uint32_t* hist = MF + NT;                           // [B]
+    uint32_t* off = hist + B;                           // [B] tile offsets
+    uint32_t* run = off + B;                            // [B] running ranks
+    uint32_t* cur = run + B;                            // [B] slab fill of this CTA
+    uint32_t* warp_tmp = cur + B;                       // [32]
+    uint16_t* stb = reinterpret_cast<uint16_t*>(warp_tmp + 32);   // [T] bucket, bucket order
+    uint16_t* sts = stb + T;                                       // [T] tile slot, bucket order
     constexpr uint64_t S = 1ull << D;
     const K gbase = ldg(p.a), gtop = ldg(p.a + p.n - 1);
     const uint32_t gsh = image_shift(gbase, gtop);
@@ -325,73 +330,113 @@ k_part(const PartParams<K> p) {
             // slot k at depth d holds sorted maximum i = (2(k - 2^d) + 1) 2^(DB-1-d) - 1
             const uint32_t d = 31u - (uint32_t)__clz((int)k);
             const uint64_t i = ((2ull * (k - (1u << d)) + 1) << (DB - 1 - d)) - 1;
-            if (i < p.B - 1) f = seg_image(ldg(p.a + (i + 1) * S - 1), gbase, gsh);
+            if (i < (uint64_t)B - 1) f = seg_image(ldg(p.a + (i + 1) * S - 1), gbase, gsh);
         }
         MF[k] = f;
     }
+    for (uint32_t b = threadIdx.x; b < B; b += blockDim.x) cur[b] = 0;
     const uint64_t pol_stream = p.stream_hint ? policy_evict_first() : policy_evict_normal();
-    const uint64_t ntiles = (p.m + kPartTile - 1) / kPartTile;
-    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        for (uint32_t i = threadIdx.x; i < NSB; i += blockDim.x) cnt[i] = 0;
-        __syncthreads();   // (also: the maxima image is complete)
-        K x[E];
-        uint32_t b[E];
-        const uint64_t base = t * kPartTile;
+    const uint64_t ntiles = (p.m + T - 1) / T;
+    const uint32_t c = blockIdx.x, G = p.G;
+    // the next tile's queries are loaded while this tile is sorted and written
+    K xn[E];
+    auto load_tile = [&](uint64_t t, K* xs) {
+        const uint64_t b0 = t * T;
 #pragma unroll
         for (uint32_t e = 0; e < E; ++e) {
-            const uint64_t i = base + e * 1024u + threadIdx.x;
-            b[e] = 0xFFFFFFFFu;
-            x[e] = 0;
-            if (i < p.m) {
-                x[e] = load_stream(p.q + i, true, pol_stream);
-                b[e] = part_bucket<K, D>(MF, DB, p.a, p.B, gbase, gsh, x[e]);
-                atomicAdd(&cnt[b[e] >> p.sbsh], 1u);
+            const uint64_t i = b0 + e * 1024u + threadIdx.x;
+            xs[e] = (t < ntiles && i < p.m) ? load_stream(p.q + i, true, pol_stream) : (K)0;
+        }
+    };
+    load_tile(c, xn);
+    for (uint64_t t = c; t < ntiles; t += G) {
+        for (uint32_t b = threadIdx.x; b < B; b += blockDim.x) { hist[b] = 0; run[b] = 0; }
+        __syncthreads();   // (also: the maxima image and cur are ready)
+        K x[E];
+        uint32_t bk[E];
+        const uint64_t base = t * T;
+        const uint32_t cnt = (uint32_t)((p.m - base) < T ? (p.m - base) : T);
+        uint32_t fx[E], kk[E];
+#pragma unroll
+        for (uint32_t e = 0; e < E; ++e) x[e] = xn[e];
+        load_tile(t + G, xn);
+#pragma unroll
+        for (uint32_t e = 0; e < E; ++e) {
+            fx[e] = seg_image(x[e], gbase, gsh);
+            kk[e] = 1;
+        }
+        // E independent descents interleaved: the shared-memory latency overlaps
+        for (uint32_t d = 0; d < DB; ++d) {
+#pragma unroll
+            for (uint32_t e = 0; e < E; ++e) kk[e] = 2u * kk[e] + (MF[kk[e]] < fx[e] ? 1u : 0u);
+        }
+#pragma unroll
+        for (uint32_t e = 0; e < E; ++e) {
+            const uint32_t j = e * 1024u + threadIdx.x;
+            bk[e] = 0xFFFFFFFFu;
+            if (j < cnt) {
+                uint32_t c = kk[e] - NT;
+                const uint32_t succ = kk[e] >> __ffs((int)~kk[e]);
+                if (succ != 0 && MF[succ] == fx[e]) c = bucket_fix<K, D>(p.a, B - 1, c, x[e]);
+                bk[e] = c;
+                atomicAdd(&hist[c], 1u);
             }
         }
         __syncthreads();
-        for (uint32_t i = threadIdx.x; i < NSB; i += blockDim.x) off[i] = cnt[i];
-        __syncthreads();
-        block_exscan(off, NSB, warp_tmp);
-        // one global reservation per (tile, bucket): the tile's records of bucket
-        // b take [gb[b], gb[b] + cnt[b]) of b's region
-        for (uint32_t i = threadIdx.x; i < NSB; i += blockDim.x) {
-            const uint32_t c = cnt[i];
-            if (exact_groups && c) gb[i] = atomicAdd(p.cursor + i, c);
-            cnt[i] = 0;
+        for (uint32_t b = threadIdx.x; b < B; b += blockDim.x) {
+            off[b] = hist[b];
+            // tile meta for the unpartition: run length and slab position per bucket
+            p.thist[t * B + b] = (uint16_t)hist[b];
+            p.tstart[t * B + b] = (uint16_t)cur[b];
         }
         __syncthreads();
+        block_exscan(off, B, warp_tmp);
 #pragma unroll
         for (uint32_t e = 0; e < E; ++e) {
-            if (b[e] == 0xFFFFFFFFu) continue;
-            const uint32_t grp = b[e] >> p.sbsh;
-            const uint32_t r = atomicAdd(&cnt[grp], 1u);
-            const uint32_t pos = off[grp] + r;
-            p.slot2[base + pos] = (uint16_t)(e * 1024u + threadIdx.x);
-            PartRec<K> rec;
-            memset(&rec, 0, sizeof rec);
-            rec.q = x[e];
-            rec.dst = (uint32_t)(base + pos);
-            const uint32_t g = exact_groups ? gb[grp] + r : atomicAdd(p.cursor + b[e], 1u);
-            if (g < p.cap) p.rec[b[e] * p.cap + g] = rec;
-            else p.ovf[atomicAdd(p.ovf_n, 1u)] = rec;
+            if (bk[e] == 0xFFFFFFFFu) continue;
+            const uint32_t pos = off[bk[e]] + atomicAdd(&run[bk[e]], 1u);
+            stq[pos] = x[e];
+            stb[pos] = (uint16_t)bk[e];
+            sts[pos] = (uint16_t)(e * 1024u + threadIdx.x);
         }
-        __syncthreads();   // cnt / off / gb are reused by the next tile
+        __syncthreads();
+        for (uint32_t j = threadIdx.x; j < cnt; j += blockDim.x) {
+            p.slot2[base + j] = sts[j];
+            p.b2[base + j] = stb[j];
+            const uint32_t b = stb[j];
+            const uint32_t g = cur[b] + (j - off[b]);
+            if (g < p.cap) {
+                p.rec[((uint64_t)b * G + c) * p.cap + g] = stq[j];
+            } else {
+                const uint32_t o = atomicAdd(p.ovf_n, 1u);
+                p.ovf_q[o] = stq[j];
+                p.ovf_j[o] = (uint32_t)(base + j);
+            }
+        }
+        __syncthreads();
+        for (uint32_t b = threadIdx.x; b < B; b += blockDim.x) {
+            const uint32_t v = cur[b] + hist[b];
+            cur[b] = v < p.cap ? v : p.cap;
+        }
     }
+    __syncthreads();
+    for (uint32_t b = threadIdx.x; b < B; b += blockDim.x) p.slabcnt[(uint64_t)c * B + b] = cur[b];
 }
 
+// Segment lookups per bucket: the bucket's G slabs, results at the same positions.
 template <class K, int D, int OB>
 __global__ void __launch_bounds__(1024, 1)
 k_seg_part(const PartParams<K> p) {
+    using O = typename std::conditional<OB == 8, uint64_t, uint32_t>::type;
     constexpr uint32_t S = 1u << D;
     extern __shared__ __align__(16) uint32_t sm[];
     uint32_t* F = sm;
-    const uint64_t G = gridDim.x, B = p.B, n = p.n;
-    // work items: bucket b split into P parts (P > 1 only when there are fewer
-    // buckets than twice the CTAs); CTA c takes items [I*c/G, I*(c+1)/G), so
-    // consecutive items of one CTA mostly share their segment
-    const uint64_t P = B >= 2 * G ? 1 : (2 * G + B - 1) / B;
+    const uint64_t GC = gridDim.x, B = p.B, n = p.n;
+    // work items: bucket b split into P parts of its slabs (P > 1 only when there
+    // are fewer buckets than twice the CTAs); consecutive items share a segment
+    const uint64_t P = B >= 2 * GC ? 1 : (2 * GC + B - 1) / B;
     const uint64_t I = B * P;
-    const uint64_t i0 = I * blockIdx.x / G, i1 = I * (blockIdx.x + 1) / G;
+    const uint64_t i0 = I * blockIdx.x / GC, i1 = I * (blockIdx.x + 1) / GC;
     uint64_t staged = ~0ull;
     for (uint64_t it = i0; it < i1; ++it) {
         const uint64_t b = it / P, part = it % P;
@@ -406,45 +451,150 @@ k_seg_part(const PartParams<K> p) {
             __syncthreads();
             staged = b;
         }
-        uint32_t cntb = p.cursor[b];
-        if (cntb > p.cap) cntb = (uint32_t)p.cap;
-        const uint32_t j0 = (uint32_t)(cntb * part / P), j1 = (uint32_t)(cntb * (part + 1) / P);
-        const PartRec<K>* rb = p.rec + b * p.cap;
-        for (uint32_t j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
-            const PartRec<K> r = rb[j];
-            bool hit;
-            const uint64_t lb = lo + seg_search<K, D>(F, seg, len, smin, sh, r.q, &hit);
-            if constexpr (OB == 8) ((uint64_t*)p.res2)[r.dst] = enc<8>(lb, hit);
-            else ((uint32_t*)p.res2)[r.dst] = (uint32_t)enc<4>(lb, hit);
+        const uint32_t c0 = (uint32_t)(p.G * part / P), c1 = (uint32_t)(p.G * (part + 1) / P);
+        // one warp per slab; R queries per lane descend together (their
+        // shared-memory and global latencies overlap)
+        constexpr uint32_t R = 4;
+        const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+        for (uint32_t c = c0 + warp; c < c1; c += nw) {
+            const uint64_t sb = ((uint64_t)b * p.G + c) * p.cap;
+            const uint32_t cnt = p.slabcnt[(uint64_t)c * B + b];
+            for (uint32_t j0 = 0; j0 < cnt; j0 += 32 * R) {
+                K x[R];
+                uint32_t k[R], fx[R];
+#pragma unroll
+                for (uint32_t r = 0; r < R; ++r) {
+                    const uint32_t j = j0 + r * 32 + lane;
+                    x[r] = j < cnt ? p.rec[sb + j] : smin;
+                    fx[r] = seg_image(x[r], smin, sh);
+                    k[r] = 1;
+                }
+#pragma unroll
+                for (int d = 0; d < D; ++d) {
+#pragma unroll
+                    for (uint32_t r = 0; r < R; ++r) k[r] = 2u * k[r] + (F[k[r]] < fx[r] ? 1u : 0u);
+                }
+                uint32_t cc[R];
+                K v[R];
+#pragma unroll
+                for (uint32_t r = 0; r < R; ++r) {
+                    cc[r] = k[r] - S;
+                    if (sh == 0) v[r] = cc[r] < len ? (K)(smin + (K)F[k[r] >> __ffs((int)~k[r])]) : (K)0;
+                    else v[r] = cc[r] < len ? ldg(seg + cc[r]) : (K)0;
+                }
+#pragma unroll
+                for (uint32_t r = 0; r < R; ++r) {
+                    const uint32_t j = j0 + r * 32 + lane;
+                    if (j >= cnt) continue;
+                    uint32_t c2 = cc[r];
+                    K vv = v[r];
+                    if (c2 < len && vv < x[r]) {
+                        if (sh == 0) {
+                            c2 = len;   // only the segment max (slot 0) can be below q
+                        } else {
+                            bool h;
+                            c2 = seg_search<K, D>(F, seg, len, smin, sh, x[r], &h);
+                            vv = c2 < len ? ldg(seg + c2) : (K)0;
+                        }
+                    }
+                    const bool hit = c2 < len && vv == x[r];
+                    ((O*)p.res)[sb + j] = (O)enc<OB>(lo + c2, hit);
+                }
+            }
         }
     }
 }
 
 template <class K, int OB>
 __global__ void k_part_ovf(const PartParams<K> p) {
+    using O = typename std::conditional<OB == 8, uint64_t, uint32_t>::type;
     const uint32_t no = *p.ovf_n;
     for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < no; j += (uint64_t)gridDim.x * blockDim.x) {
-        const PartRec<K> r = p.ovf[j];
-        const uint64_t lb = lower_bound_global(p.a, p.n, r.q);
-        const bool hit = lb < p.n && ldg(p.a + lb) == r.q;
-        if constexpr (OB == 8) ((uint64_t*)p.res2)[r.dst] = enc<8>(lb, hit);
-        else ((uint32_t*)p.res2)[r.dst] = (uint32_t)enc<4>(lb, hit);
+        const K x = p.ovf_q[j];
+        const uint64_t lb = lower_bound_global(p.a, p.n, x);
+        const bool hit = lb < p.n && ldg(p.a + lb) == x;
+        ((O*)p.res_full)[p.ovf_j[j]] = (O)enc<OB>(lb, hit);
     }
 }
 
+// Unpartition: per tile (on CTA t % G, in the partition's tile order, so each
+// slab line is read while L2 still holds it) gather the tile's results run by
+// run, scatter them to query order in shared memory, one coalesced store.
+constexpr uint32_t kUnpartThreads = 1024;
+
+// Unpartition: per tile (tile t's runs sit in the slabs of owner t % G) gather
+// the tile's results run by run, scatter them to query order in shared memory,
+// store the tile coalesced.  The next tile's meta (run lengths, slab positions)
+// and its (bucket, slot) lists are loaded while this tile is gathered.
 template <class K, int OB>
-__global__ void __launch_bounds__(1024, 1)
+__global__ void __launch_bounds__(kUnpartThreads, 1)
 k_unpart(const PartParams<K> p) {
     using O = typename std::conditional<OB == 8, uint64_t, uint32_t>::type;
+    constexpr uint32_t T = kPartTile, E = T / kUnpartThreads;
+    constexpr uint32_t MB = kGlobMaxB / kUnpartThreads;   // meta entries per thread
     extern __shared__ __align__(16) uint32_t sm[];
-    O* tile = reinterpret_cast<O*>(sm);
+    const uint32_t B = p.B, G = p.G;
+    O* tile = reinterpret_cast<O*>(sm);                 // [T]
+    uint32_t* off = reinterpret_cast<uint32_t*>(tile + T);   // [B] run start in the tile's bucket order
+    uint32_t* src = off + B;                            // [B] run start in the slab
+    uint32_t* lim = src + B;                            // [B] stored run length (the rest overflowed)
+    uint32_t* warp_tmp = lim + B;                       // [32]
     const uint64_t pol_stream = p.stream_hint ? policy_evict_first() : policy_evict_normal();
-    const uint64_t ntiles = (p.m + kPartTile - 1) / kPartTile;
+    const uint64_t ntiles = (p.m + T - 1) / T;
+    uint32_t nh[MB], ns[MB], nb[E], nsl[E];
+    auto prefetch = [&](uint64_t t) {
+        if (t >= ntiles) return;
+        const uint64_t base = t * T;
+        const uint32_t cnt = (uint32_t)((p.m - base) < T ? (p.m - base) : T);
+#pragma unroll
+        for (uint32_t i = 0; i < MB; ++i) {
+            const uint32_t b = i * kUnpartThreads + threadIdx.x;
+            nh[i] = b < B ? p.thist[t * B + b] : 0u;
+            ns[i] = b < B ? p.tstart[t * B + b] : 0u;
+        }
+#pragma unroll
+        for (uint32_t e = 0; e < E; ++e) {
+            const uint32_t j = e * kUnpartThreads + threadIdx.x;
+            nb[e] = j < cnt ? p.b2[base + j] : 0u;
+            nsl[e] = j < cnt ? p.slot2[base + j] : 0u;
+        }
+    };
+    prefetch(blockIdx.x);
     for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const uint64_t base = t * kPartTile;
-        const uint32_t cnt = (uint32_t)((p.m - base) < kPartTile ? (p.m - base) : kPartTile);
-        for (uint32_t j = threadIdx.x; j < cnt; j += blockDim.x)
-            tile[p.slot2[base + j]] = ((const O*)p.res2)[base + j];
+        const uint64_t base = t * T;
+        const uint32_t cnt = (uint32_t)((p.m - base) < T ? (p.m - base) : T);
+        const uint32_t c = (uint32_t)(t % G);
+#pragma unroll
+        for (uint32_t i = 0; i < MB; ++i) {
+            const uint32_t b = i * kUnpartThreads + threadIdx.x;
+            if (b < B) {
+                off[b] = nh[i];
+                src[b] = ns[i];
+                lim[b] = ns[i] + nh[i] <= p.cap ? nh[i] : p.cap - ns[i];
+            }
+        }
+        uint32_t bb[E], sl[E];
+#pragma unroll
+        for (uint32_t e = 0; e < E; ++e) { bb[e] = nb[e]; sl[e] = nsl[e]; }
+        prefetch(t + gridDim.x);
+        __syncthreads();
+        block_exscan(off, B, warp_tmp);
+        O v[E];
+#pragma unroll
+        for (uint32_t e = 0; e < E; ++e) {
+            const uint32_t j = e * kUnpartThreads + threadIdx.x;
+            if (j < cnt) {
+                const uint32_t b = bb[e], r = j - off[b];
+                const O* sp = r < lim[b] ? (const O*)p.res + (((uint64_t)b * G + c) * p.cap + src[b] + r)
+                                         : (const O*)p.res_full + (base + j);
+                v[e] = *sp;
+            }
+        }
+#pragma unroll
+        for (uint32_t e = 0; e < E; ++e) {
+            const uint32_t j = e * kUnpartThreads + threadIdx.x;
+            if (j < cnt) tile[sl[e]] = v[e];
+        }
         __syncthreads();
         for (uint32_t j = threadIdx.x; j < cnt; j += blockDim.x)
             store_stream((O*)p.out + base + j, tile[j], true, pol_stream);
@@ -491,68 +641,86 @@ cudaError_t launch_seg_sorted(int kb, int ob, const void* a, uint64_t n, const v
 
 // workspace layout of the GLOBAL mode (all offsets 256-B aligned)
 struct PartLayout {
-    uint64_t B, cap, o_cursor, o_rec, o_ovf, o_res2, o_slot2, total;
+    uint64_t B, G, cap, ntiles;
+    uint64_t o_rec, o_res, o_slot2, o_b2, o_thist, o_tstart, o_slabcnt, o_ovfn, o_ovfq, o_ovfj, o_resfull, total;
 };
 
 static uint64_t al256(uint64_t x) { return (x + 255) & ~255ull; }
 
-static bool part_layout(uint64_t n, uint64_t m, int kb, int ob, PartLayout* L) {
-    const uint64_t S = 1ull << kSegLog2;
+static bool part_layout(uint64_t n, uint64_t m, int kb, int ob, uint32_t G, PartLayout* L) {
+    const uint64_t S = 1ull << kGlobLog2;
     L->B = (n + S - 1) / S;
-    if (L->B > (1ull << kPartMaxLog2B) || m >= (1ull << 32)) return false;
-    L->cap = (m + L->B - 1) / L->B;
-    L->cap += L->cap / 4 + 64;
-    const uint64_t rs = kb == 8 ? 16 : 8;
+    L->G = G;
+    if (L->B > kGlobMaxB || m >= (1ull << 32)) return false;
     const uint64_t mm = m ? m : 1;
-    L->o_cursor = 0;
-    L->o_rec = al256(4 * (L->B + 1));
-    L->o_ovf = L->o_rec + al256(rs * L->B * L->cap);
-    L->o_res2 = L->o_ovf + al256(rs * mm);
-    L->o_slot2 = L->o_res2 + al256((uint64_t)ob * mm);
-    L->total = L->o_slot2 + al256(2 * mm);
+    L->ntiles = (mm + kPartTile - 1) / kPartTile;
+    uint64_t cap = (mm + L->B * G - 1) / (L->B * G);   // expected queries per slab
+    cap += cap / 4 + 64;                                 // + slack (beyond: the overflow list)
+    if (cap > 65535) cap = 65535;
+    L->cap = cap;
+    const uint64_t slots = L->B * G * cap;
+    uint64_t o = 0;
+    auto take = [&](uint64_t bytes) { const uint64_t r = o; o += al256(bytes); return r; };
+    L->o_rec = take(slots * kb);
+    L->o_res = take(slots * ob);
+    L->o_slot2 = take(2 * mm);
+    L->o_b2 = take(2 * mm);
+    L->o_thist = take(2 * L->ntiles * L->B);
+    L->o_tstart = take(2 * L->ntiles * L->B);
+    L->o_slabcnt = take(4 * G * L->B);
+    L->o_ovfn = take(4);
+    L->o_ovfq = take(kb * mm);
+    L->o_ovfj = take(4 * mm);
+    L->o_resfull = take((uint64_t)ob * mm);
+    L->total = o;
     return true;
 }
 
-bool part_workspace_bytes(uint64_t n, uint64_t m, int kb, int ob, uint64_t* bytes) {
+bool part_workspace_bytes(uint64_t n, uint64_t m, int kb, int ob, uint32_t sm_count, uint64_t* bytes) {
     PartLayout L;
-    if (!part_layout(n, m, kb, ob, &L)) return false;
+    if (!part_layout(n, m, kb, ob, sm_count, &L)) return false;
     *bytes = L.total;
     return true;
 }
 
 template <class K, int OB>
 static cudaError_t go_part(PartParams<K> p, const PartLayout& L, char* ws, uint32_t sm_count, cudaStream_t s) {
-    constexpr int D = kSegLog2;
-    p.cursor = (uint32_t*)(ws + L.o_cursor);
-    p.ovf_n = p.cursor + L.B;
-    p.rec = (PartRec<K>*)(ws + L.o_rec);
-    p.ovf = (PartRec<K>*)(ws + L.o_ovf);
-    p.res2 = ws + L.o_res2;
+    constexpr int D = kGlobLog2;
+    p.B = (uint32_t)L.B;
+    p.G = (uint32_t)L.G;
+    p.cap = (uint32_t)L.cap;
+    p.rec = (K*)(ws + L.o_rec);
+    p.res = ws + L.o_res;
     p.slot2 = (uint16_t*)(ws + L.o_slot2);
-    p.B = L.B;
-    p.cap = L.cap;
+    p.b2 = (uint16_t*)(ws + L.o_b2);
+    p.thist = (uint16_t*)(ws + L.o_thist);
+    p.tstart = (uint16_t*)(ws + L.o_tstart);
+    p.slabcnt = (uint32_t*)(ws + L.o_slabcnt);
+    p.ovf_n = (uint32_t*)(ws + L.o_ovfn);
+    p.ovf_q = (K*)(ws + L.o_ovfq);
+    p.ovf_j = (uint32_t*)(ws + L.o_ovfj);
+    p.res_full = ws + L.o_resfull;
     uint32_t lb = 0;
     while ((1ull << lb) < L.B) ++lb;
     p.DB = lb ? lb : 1;
-    p.sbsh = lb > kPartLog2SB ? lb - kPartLog2SB : 0;
-    const uint32_t nsb = (uint32_t)((L.B - 1) >> p.sbsh) + 1;
-    cudaError_t e = cudaMemsetAsync(p.cursor, 0, 4 * (L.B + 1), s);
+    cudaError_t e = cudaMemsetAsync(p.ovf_n, 0, 4, s);
     if (e != cudaSuccess) return e;
-    Grid grid{1u, 1u, sm_count};
     bool uns = false;
     uint64_t g = 0;
-    {   // partition
+    {   // partition: exactly G CTAs (tile t on CTA t % G; the unpartition relies on it)
         auto kern = k_part<K, D>;
-        const uint32_t smem = 4u * ((1u << p.DB) + 3u * nsb + 32u);
-        e = plan_grid((const void*)kern, 1024, smem, grid, sm_count, carveout_for(smem, 1024), &g, &uns);
+        const uint32_t smem = kPartTile * (uint32_t)sizeof(K) + 4u * ((1u << p.DB) + 4u * p.B + 32u) + 4u * kPartTile;
+        Grid grid{1u, 1u, p.G};
+        e = plan_grid((const void*)kern, 1024, smem, grid, p.G, carveout_for(smem, 1024), &g, &uns);
         if (e != cudaSuccess) return e;
-        if (uns) return cudaErrorInvalidConfiguration;
+        if (uns || g != p.G) return cudaErrorInvalidConfiguration;
         kern<<<(unsigned)g, 1024, smem, s>>>(p);
         count_launch();
     }
     {   // segment lookups per bucket
         auto kern = k_seg_part<K, D, OB>;
         const uint32_t smem = 4u << D;
+        Grid grid{1u, 1u, sm_count};
         e = plan_grid((const void*)kern, 1024, smem, grid, sm_count, carveout_for(smem, 1024), &g, &uns);
         if (e != cudaSuccess) return e;
         if (uns) return cudaErrorInvalidConfiguration;
@@ -561,14 +729,15 @@ static cudaError_t go_part(PartParams<K> p, const PartLayout& L, char* ws, uint3
     }
     k_part_ovf<K, OB><<<sm_count, 256, 0, s>>>(p);
     count_launch();
-    {   // back to query order
+    {   // back to query order (slab owner = tile % G is an address, not a CTA)
         auto kern = k_unpart<K, OB>;
-        const uint32_t smem = kPartTile * OB;
-        Grid g2{1u, 0u, sm_count};
-        e = plan_grid((const void*)kern, 1024, smem, g2, (p.m + kPartTile - 1) / kPartTile, carveout_for(smem, 1024), &g, &uns);
+        const uint32_t smem = kPartTile * OB + 4u * (3u * p.B + 32u);
+        Grid grid{1u, 1u, sm_count};
+        e = plan_grid((const void*)kern, kUnpartThreads, smem, grid, sm_count, carveout_for(smem, kUnpartThreads),
+                      &g, &uns);
         if (e != cudaSuccess) return e;
         if (uns) return cudaErrorInvalidConfiguration;
-        kern<<<(unsigned)g, 1024, smem, s>>>(p);
+        kern<<<(unsigned)g, kUnpartThreads, smem, s>>>(p);
         count_launch();
     }
     return cudaGetLastError();
@@ -578,7 +747,7 @@ cudaError_t launch_part_global(int kb, int ob, const void* a, uint64_t n, const 
                                uint32_t stream_hint, void* ws, uint64_t ws_bytes, uint32_t sm_count, cudaStream_t s,
                                bool* uns) {
     PartLayout L;
-    if (!part_layout(n, m, kb, ob, &L) || ws_bytes < L.total) { *uns = true; return cudaSuccess; }
+    if (!part_layout(n, m, kb, ob, sm_count, &L) || ws_bytes < L.total) { *uns = true; return cudaSuccess; }
     if (kb == 8) {
         PartParams<uint64_t> p{};
         p.a = (const uint64_t*)a; p.n = n; p.m = m; p.q = (const uint64_t*)q; p.out = out; p.stream_hint = stream_hint;

@@ -100,7 +100,8 @@ def glob_run(idx, q, ob):
 @pytest.mark.parametrize("kb", [4, 8])
 @pytest.mark.parametrize("order", ["random", "sorted"])
 def test_global_edge_sizes(kb, order):
-    for t, n in enumerate([1, 2, 100, S - 1, S, S + 1, 3 * S + 5, 100003]):
+    SG = 32768   # GLOBAL mode bucket segment (seg.cu kGlobLog2)
+    for t, n in enumerate([1, 2, 100, S + 1, SG - 1, SG, SG + 1, 3 * SG + 5, 300007]):
         keys = workload.gen_keys(n, kb, seed=500 + t)
         for m in (1, 777, 8191, 8192, 8193, 30011):
             q = queries_for(keys, m, 600 + t, order)
@@ -113,20 +114,21 @@ def test_global_edge_sizes(kb, order):
 @pytest.mark.parametrize("kind", ["dups", "narrow", "clustered", "top"])
 def test_global_key_distributions(kind):
     rng = np.random.default_rng({"dups": 11, "narrow": 12, "clustered": 13, "top": 14}[kind])
-    n = 5 * S + 77
+    SG = 32768
+    n = 5 * SG + 77
     if kind == "dups":
         v = np.repeat(rng.integers(0, 1 << 62, size=n // 40, dtype=np.uint64), 40)
-        v = np.concatenate([v, np.full(2 * S + 3, 1 << 61, dtype=np.uint64)])
+        v = np.concatenate([v, np.full(2 * SG + 3, 1 << 61, dtype=np.uint64)])
     elif kind == "narrow":
         v = rng.integers(0, 1 << 32, size=n, dtype=np.uint64)
     elif kind == "clustered":
         v = np.concatenate([rng.integers(0, 1 << 20, size=n // 2, dtype=np.uint64),
                             rng.integers(0, 1 << 63, size=n // 2, dtype=np.uint64) * np.uint64(2)])
     else:
-        v = np.concatenate([np.full(S + 9, (1 << 64) - 1, dtype=np.uint64),
+        v = np.concatenate([np.full(SG + 9, (1 << 64) - 1, dtype=np.uint64),
                             rng.integers((1 << 64) - (1 << 40), (1 << 64) - 1, size=n, dtype=np.uint64)])
     keys = np.sort(v)
-    q = queries_for(keys, 60000, 8, "random")
+    q = queries_for(keys, 200000, 8, "random")
     idx = build(keys, variant=bs.KARY, out_bytes=8)
     check(glob_run(idx, q, 8), oracle.lookup(keys, q, out_bytes=8), q, kind)
     idx.close()
@@ -135,8 +137,8 @@ def test_global_key_distributions(kind):
 def test_global_skewed_batch_overflows():
     """Every query in one segment: its region overflows (cap = 1.25 m/B + 64) and
     the overflow list is looked up by global bisection — same results."""
-    keys = workload.gen_keys(6 * S, 8, seed=21)
-    hot = keys[2 * S: 2 * S + 50]
+    keys = workload.gen_keys(6 * 32768, 8, seed=21)
+    hot = keys[2 * 32768: 2 * 32768 + 50]
     rng = np.random.default_rng(3)
     q = np.concatenate([rng.choice(hot, 40000), workload.gen_queries(keys, 5000, seed=4)])
     q = q[rng.permutation(q.size)]

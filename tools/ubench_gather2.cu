@@ -116,7 +116,7 @@ int main(int argc, char** argv) {
     const int blocks = sms * 8;
     int row = 0;
 #define ROW(...) if (only < 0 || only == row) { __VA_ARGS__; } ++row;
-    for (uint64_t bytes : {512ull << 20, 8ull << 30}) {
+    for (uint64_t bytes : {32ull << 20, 512ull << 20, 8ull << 30}) {
         ROW((run<32, 8, false, false>(buf, bytes, blocks, 16, qin, qout, sink, 1)))
         ROW((run<64, 8, false, false>(buf, bytes, blocks, 16, qin, qout, sink, 1)))
         ROW((run<128, 4, false, false>(buf, bytes, blocks, 16, qin, qout, sink, 1)))
