@@ -200,7 +200,8 @@ int bs_launch_default(const void* idx, bs_launch* l);
  *   n        >= 1 (P:65 needs n-1 >= 0); out_bytes = 4 requires n < 2^31.
  *   layout   see bs_layout; NULL = bs_layout_default().
  *   out_idx  receives the index; NULL on error.
- * Synchronous: returns when the index is ready.  Always builds the pinned
+ * Synchronous: waits for all prior work on the device (the keys may have been
+ * produced on any stream), returns when the index is ready.  Always builds the pinned
  * table for OPT and the separator levels for KARY; the NAIVE variant needs
  * neither.  Errors: BS_ERR_INVALID (NULL pointers, n == 0, bad widths, K not
  * in [2,33], C not a power of two in [1,256], nonzero reserved fields),

@@ -449,6 +449,10 @@ int bs_build(const void* keys, uint64_t n, const bs_layout* layout_in, void** ou
 
     e = cudaGetDevice(&ix->device);
     if (e != cudaSuccess) { rc = fail_cuda(e, "cudaGetDevice"); goto done; }
+    // the caller's keys may still be in flight on any of its streams (bs_build
+    // takes no stream): wait for the device before reading them
+    e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) { rc = fail_cuda(e, "bs_build: device synchronisation"); goto done; }
     {
         int v = 0;
         cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, ix->device); ix->sm_count = v;

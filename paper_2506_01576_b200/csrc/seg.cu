@@ -212,6 +212,8 @@ constexpr int kSegLog2 = 13;           // SORTED: S = 8192 keys per segment (a 3
 constexpr int kGlobLog2 = 15;          // GLOBAL: S = 32768 keys per bucket segment (a 128-KB image)
 constexpr uint32_t kPartTile = 8192;   // queries per partition tile (u16 positions)
 constexpr uint32_t kGlobMaxB = 2048;   // buckets (n <= 2^26 keys): per-bucket counters fit shared memory
+constexpr uint32_t kPartBins = 8192;   // radix directory over the 31-bit maxima images
+constexpr uint32_t kPartBinShift = 18; // 2^31 >> 18 = kPartBins
 
 // Slab layout: bucket b's region holds one slab of `cap` queries per partition
 // CTA c (slab(b, c) = (b * G + c) * cap), filled in tile order by that CTA
@@ -231,7 +233,8 @@ struct PartParams {
     void* res;                // [B * G * cap] their results (same positions)
     uint16_t* slot2;          // [m] tile slot of the tile's j-th query in bucket order
     uint16_t* b2;             // [m] its bucket
-    uint16_t* thist;          // [ntiles * B] queries of bucket b in tile t
+    uint16_t* toff;           // [ntiles * B] start of bucket b's run in tile t's bucket order
+    uint16_t* tlim;           // [ntiles * B] length of that run stored in the slab (the rest overflowed)
     uint16_t* tstart;         // [ntiles * B] position of tile t's run in slab(b, t % G)
     uint32_t* slabcnt;        // [G * B] queries stored per slab
     uint32_t* ovf_n;          // overflowed queries (slab full: a skewed batch)
@@ -312,27 +315,37 @@ k_part(const PartParams<K> p) {
     constexpr uint32_t T = kPartTile, E = T / 1024;
     extern __shared__ __align__(16) uint32_t sm[];
     const uint32_t B = p.B, DB = p.DB, NT = 1u << DB;
-    K* stq = reinterpret_cast<K*>(sm);                 // [T] queries in bucket order
-    uint32_t* MF = reinterpret_cast<uint32_t*>(stq + T);   // [NT] maxima image (Eytzinger)
-    uint32_t* hist = MF + NT;                           // [B]
-    uint32_t* off = hist + B;                           // [B] tile offsets
-    uint32_t* run = off + B;                            // [B] running ranks
-    uint32_t* cur = run + B;                            // [B] slab fill of this CTA
-    uint32_t* warp_tmp = cur + B;                       // [32]
-    uint16_t* stb = reinterpret_cast<uint16_t*>(warp_tmp + 32);   // [T] bucket, bucket order
+    const uint32_t B4 = (B + 3u) & ~3u;                     // per-bucket arrays padded to 16 B
+    K* stq = reinterpret_cast<K*>(sm);                      // [T] queries in bucket order
+    uint64_t* dptr = reinterpret_cast<uint64_t*>(stq + T);  // [B] rec index of run position 0 (minus off)
+    uint32_t* MS = reinterpret_cast<uint32_t*>(dptr + B4);  // [B] maxima images, sorted (MS[B-1] = max)
+    uint32_t* hist = MS + B4;                               // [B]
+    uint32_t* off = hist + B4;                              // [B] tile offsets
+    uint32_t* run = off + B4;                               // [B] running ranks, then the fitting limit
+    uint32_t* cur = run + B4;                               // [B] slab fill of this CTA
+    uint32_t* warp_tmp = cur + B4;                          // [32]
+    uint16_t* BF = reinterpret_cast<uint16_t*>(warp_tmp + 32);    // [kPartBins + 8] bin -> first bucket
+    uint16_t* stb = BF + kPartBins + 8;                            // [T] bucket, bucket order (8-B aligned)
     uint16_t* sts = stb + T;                                       // [T] tile slot, bucket order
     constexpr uint64_t S = 1ull << D;
     const K gbase = ldg(p.a), gtop = ldg(p.a + p.n - 1);
     const uint32_t gsh = image_shift(gbase, gtop);
-    for (uint32_t k = threadIdx.x; k < NT; k += blockDim.x) {
-        uint32_t f = 0xFFFFFFFFu;
-        if (k > 0) {
-            // slot k at depth d holds sorted maximum i = (2(k - 2^d) + 1) 2^(DB-1-d) - 1
-            const uint32_t d = 31u - (uint32_t)__clz((int)k);
-            const uint64_t i = ((2ull * (k - (1u << d)) + 1) << (DB - 1 - d)) - 1;
-            if (i < (uint64_t)B - 1) f = seg_image(ldg(p.a + (i + 1) * S - 1), gbase, gsh);
+    // bucket b(q) = #(maxima < q): the maxima's order-preserving images, sorted,
+    // and a radix directory over the images' top bits (the partition is one
+    // radix-style pass over key ranges): bin x of image f = f >> kPartBinShift
+    // holds the buckets [BF[x], BF[x+1]], usually one compare
+    for (uint32_t i = threadIdx.x; i < B; i += blockDim.x)
+        MS[i] = i + 1 < B ? seg_image(ldg(p.a + ((uint64_t)i + 1) * S - 1), gbase, gsh) : 0xFFFFFFFFu;
+    __syncthreads();
+    for (uint32_t x = threadIdx.x; x <= kPartBins + 1; x += blockDim.x) {
+        const uint64_t f = (uint64_t)x << kPartBinShift;   // first image of bin x
+        uint32_t lo = 0, hi = B - 1;                       // #(MS[c] < f) over the B-1 real maxima
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if ((uint64_t)MS[mid] < f) lo = mid + 1;
+            else hi = mid;
         }
-        MF[k] = f;
+        BF[x] = (uint16_t)lo;
     }
     for (uint32_t b = threadIdx.x; b < B; b += blockDim.x) cur[b] = 0;
     const uint64_t pol_stream = p.stream_hint ? policy_evict_first() : policy_evict_normal();
@@ -342,10 +355,14 @@ k_part(const PartParams<K> p) {
     K xn[E];
     auto load_tile = [&](uint64_t t, K* xs) {
         const uint64_t b0 = t * T;
+        const K* qp = p.q + b0 + threadIdx.x;
+        if (b0 + T <= p.m) {
 #pragma unroll
-        for (uint32_t e = 0; e < E; ++e) {
-            const uint64_t i = b0 + e * 1024u + threadIdx.x;
-            xs[e] = (t < ntiles && i < p.m) ? load_stream(p.q + i, true, pol_stream) : (K)0;
+            for (uint32_t e = 0; e < E; ++e) xs[e] = load_stream(qp + e * 1024u, true, pol_stream);
+        } else {
+#pragma unroll
+            for (uint32_t e = 0; e < E; ++e)
+                xs[e] = (b0 + e * 1024u + threadIdx.x < p.m) ? load_stream(qp + e * 1024u, true, pol_stream) : (K)0;
         }
     };
     load_tile(c, xn);
@@ -356,41 +373,47 @@ k_part(const PartParams<K> p) {
         uint32_t bk[E];
         const uint64_t base = t * T;
         const uint32_t cnt = (uint32_t)((p.m - base) < T ? (p.m - base) : T);
-        uint32_t fx[E], kk[E];
+        uint32_t fx[E], lo[E], hi[E];
 #pragma unroll
         for (uint32_t e = 0; e < E; ++e) x[e] = xn[e];
-        load_tile(t + G, xn);
+        if (t + G < ntiles) load_tile(t + G, xn);
 #pragma unroll
         for (uint32_t e = 0; e < E; ++e) {
             fx[e] = seg_image(x[e], gbase, gsh);
-            kk[e] = 1;
-        }
-        // E independent descents interleaved: the shared-memory latency overlaps
-        for (uint32_t d = 0; d < DB; ++d) {
-#pragma unroll
-            for (uint32_t e = 0; e < E; ++e) kk[e] = 2u * kk[e] + (MF[kk[e]] < fx[e] ? 1u : 0u);
+            const uint32_t bin = fx[e] >> kPartBinShift;
+            lo[e] = BF[bin];
+            hi[e] = BF[bin + 1];
         }
 #pragma unroll
         for (uint32_t e = 0; e < E; ++e) {
             const uint32_t j = e * 1024u + threadIdx.x;
             bk[e] = 0xFFFFFFFFu;
             if (j < cnt) {
-                uint32_t c = kk[e] - NT;
-                const uint32_t succ = kk[e] >> __ffs((int)~kk[e]);
-                if (succ != 0 && MF[succ] == fx[e]) c = bucket_fix<K, D>(p.a, B - 1, c, x[e]);
-                bk[e] = c;
-                atomicAdd(&hist[c], 1u);
+                // #(maxima with image < fx) lies in [lo, hi]: step (bisect when the bin is crowded)
+                uint32_t l = lo[e], h = hi[e];
+                while (h - l > 4) {
+                    const uint32_t mid = (l + h) >> 1;
+                    if (MS[mid] < fx[e]) l = mid + 1;
+                    else h = mid;
+                }
+                while (l < h && MS[l] < fx[e]) ++l;
+                uint32_t b = l;
+                if (b < B - 1 && MS[b] == fx[e]) b = bucket_fix<K, D>(p.a, B - 1, b, x[e]);
+                bk[e] = b;
+                atomicAdd(&hist[b], 1u);
             }
         }
         __syncthreads();
-        for (uint32_t b = threadIdx.x; b < B; b += blockDim.x) {
-            off[b] = hist[b];
-            // tile meta for the unpartition: run length and slab position per bucket
-            p.thist[t * B + b] = (uint16_t)hist[b];
-            p.tstart[t * B + b] = (uint16_t)cur[b];
-        }
+        for (uint32_t b = threadIdx.x; b < B; b += blockDim.x) off[b] = hist[b];
         __syncthreads();
         block_exscan(off, B, warp_tmp);
+        // tile meta for the unpartition: run start, stored length and slab position per bucket
+        for (uint32_t b = threadIdx.x; b < B; b += blockDim.x) {
+            const uint32_t room = p.cap - cur[b];
+            p.toff[t * B + b] = (uint16_t)off[b];
+            p.tlim[t * B + b] = (uint16_t)(hist[b] < room ? hist[b] : room);
+            p.tstart[t * B + b] = (uint16_t)cur[b];
+        }
 #pragma unroll
         for (uint32_t e = 0; e < E; ++e) {
             if (bk[e] == 0xFFFFFFFFu) continue;
@@ -400,16 +423,29 @@ k_part(const PartParams<K> p) {
             sts[pos] = (uint16_t)(e * 1024u + threadIdx.x);
         }
         __syncthreads();
+        // per bucket: where run position j lands in the slab, and how much of the run fits
+        for (uint32_t b = threadIdx.x; b < B; b += blockDim.x) {
+            dptr[b] = ((uint64_t)b * G + c) * p.cap + cur[b] - off[b];
+            run[b] = off[b] + (p.cap - cur[b]);
+        }
+        // the tile's (slot, bucket) lists in bucket order: 8-B vector copies
+        for (uint32_t j4 = threadIdx.x * 4; j4 < cnt; j4 += blockDim.x * 4) {
+            if (j4 + 4 <= cnt) {
+                *reinterpret_cast<uint2*>(p.slot2 + base + j4) = *reinterpret_cast<const uint2*>(sts + j4);
+                *reinterpret_cast<uint2*>(p.b2 + base + j4) = *reinterpret_cast<const uint2*>(stb + j4);
+            } else {
+                for (uint32_t j = j4; j < cnt; ++j) { p.slot2[base + j] = sts[j]; p.b2[base + j] = stb[j]; }
+            }
+        }
+        __syncthreads();
         for (uint32_t j = threadIdx.x; j < cnt; j += blockDim.x) {
-            p.slot2[base + j] = sts[j];
-            p.b2[base + j] = stb[j];
             const uint32_t b = stb[j];
-            const uint32_t g = cur[b] + (j - off[b]);
-            if (g < p.cap) {
-                p.rec[((uint64_t)b * G + c) * p.cap + g] = stq[j];
+            const K xq = stq[j];
+            if (j < run[b]) {
+                p.rec[dptr[b] + j] = xq;
             } else {
                 const uint32_t o = atomicAdd(p.ovf_n, 1u);
-                p.ovf_q[o] = stq[j];
+                p.ovf_q[o] = xq;
                 p.ovf_j[o] = (uint32_t)(base + j);
             }
         }
@@ -524,8 +560,9 @@ constexpr uint32_t kUnpartThreads = 1024;
 
 // Unpartition: per tile (tile t's runs sit in the slabs of owner t % G) gather
 // the tile's results run by run, scatter them to query order in shared memory,
-// store the tile coalesced.  The next tile's meta (run lengths, slab positions)
-// and its (bucket, slot) lists are loaded while this tile is gathered.
+// store the tile coalesced.  The next tile's meta (run start, stored length,
+// slab position per bucket) and its (bucket, slot) lists are loaded while this
+// tile is gathered.
 template <class K, int OB>
 __global__ void __launch_bounds__(kUnpartThreads, 1)
 k_unpart(const PartParams<K> p) {
@@ -534,23 +571,24 @@ k_unpart(const PartParams<K> p) {
     constexpr uint32_t MB = kGlobMaxB / kUnpartThreads;   // meta entries per thread
     extern __shared__ __align__(16) uint32_t sm[];
     const uint32_t B = p.B, G = p.G;
-    O* tile = reinterpret_cast<O*>(sm);                 // [T]
+    O* tile = reinterpret_cast<O*>(sm);                      // [T]
     uint32_t* off = reinterpret_cast<uint32_t*>(tile + T);   // [B] run start in the tile's bucket order
-    uint32_t* src = off + B;                            // [B] run start in the slab
-    uint32_t* lim = src + B;                            // [B] stored run length (the rest overflowed)
-    uint32_t* warp_tmp = lim + B;                       // [32]
+    uint32_t* src = off + B;                                 // [B] run start in the slab
+    uint32_t* lim = src + B;                                 // [B] stored run length
     const uint64_t pol_stream = p.stream_hint ? policy_evict_first() : policy_evict_normal();
     const uint64_t ntiles = (p.m + T - 1) / T;
-    uint32_t nh[MB], ns[MB], nb[E], nsl[E];
+    uint32_t no[MB], ns[MB], nl[MB], nb[E], nsl[E];
     auto prefetch = [&](uint64_t t) {
-        if (t >= ntiles) return;
         const uint64_t base = t * T;
         const uint32_t cnt = (uint32_t)((p.m - base) < T ? (p.m - base) : T);
 #pragma unroll
         for (uint32_t i = 0; i < MB; ++i) {
             const uint32_t b = i * kUnpartThreads + threadIdx.x;
-            nh[i] = b < B ? p.thist[t * B + b] : 0u;
-            ns[i] = b < B ? p.tstart[t * B + b] : 0u;
+            if (b < B) {
+                no[i] = p.toff[t * B + b];
+                nl[i] = p.tlim[t * B + b];
+                ns[i] = p.tstart[t * B + b];
+            }
         }
 #pragma unroll
         for (uint32_t e = 0; e < E; ++e) {
@@ -559,7 +597,7 @@ k_unpart(const PartParams<K> p) {
             nsl[e] = j < cnt ? p.slot2[base + j] : 0u;
         }
     };
-    prefetch(blockIdx.x);
+    if (blockIdx.x < ntiles) prefetch(blockIdx.x);
     for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const uint64_t base = t * T;
         const uint32_t cnt = (uint32_t)((p.m - base) < T ? (p.m - base) : T);
@@ -567,18 +605,13 @@ k_unpart(const PartParams<K> p) {
 #pragma unroll
         for (uint32_t i = 0; i < MB; ++i) {
             const uint32_t b = i * kUnpartThreads + threadIdx.x;
-            if (b < B) {
-                off[b] = nh[i];
-                src[b] = ns[i];
-                lim[b] = ns[i] + nh[i] <= p.cap ? nh[i] : p.cap - ns[i];
-            }
+            if (b < B) { off[b] = no[i]; src[b] = ns[i]; lim[b] = nl[i]; }
         }
         uint32_t bb[E], sl[E];
 #pragma unroll
         for (uint32_t e = 0; e < E; ++e) { bb[e] = nb[e]; sl[e] = nsl[e]; }
-        prefetch(t + gridDim.x);
+        if (t + gridDim.x < ntiles) prefetch(t + gridDim.x);
         __syncthreads();
-        block_exscan(off, B, warp_tmp);
         O v[E];
 #pragma unroll
         for (uint32_t e = 0; e < E; ++e) {
@@ -598,7 +631,6 @@ k_unpart(const PartParams<K> p) {
         __syncthreads();
         for (uint32_t j = threadIdx.x; j < cnt; j += blockDim.x)
             store_stream((O*)p.out + base + j, tile[j], true, pol_stream);
-        __syncthreads();
     }
 }
 
@@ -642,7 +674,7 @@ cudaError_t launch_seg_sorted(int kb, int ob, const void* a, uint64_t n, const v
 // workspace layout of the GLOBAL mode (all offsets 256-B aligned)
 struct PartLayout {
     uint64_t B, G, cap, ntiles;
-    uint64_t o_rec, o_res, o_slot2, o_b2, o_thist, o_tstart, o_slabcnt, o_ovfn, o_ovfq, o_ovfj, o_resfull, total;
+    uint64_t o_rec, o_res, o_slot2, o_b2, o_toff, o_tlim, o_tstart, o_slabcnt, o_ovfn, o_ovfq, o_ovfj, o_resfull, total;
 };
 
 static uint64_t al256(uint64_t x) { return (x + 255) & ~255ull; }
@@ -665,7 +697,8 @@ static bool part_layout(uint64_t n, uint64_t m, int kb, int ob, uint32_t G, Part
     L->o_res = take(slots * ob);
     L->o_slot2 = take(2 * mm);
     L->o_b2 = take(2 * mm);
-    L->o_thist = take(2 * L->ntiles * L->B);
+    L->o_toff = take(2 * L->ntiles * L->B);
+    L->o_tlim = take(2 * L->ntiles * L->B);
     L->o_tstart = take(2 * L->ntiles * L->B);
     L->o_slabcnt = take(4 * G * L->B);
     L->o_ovfn = take(4);
@@ -693,7 +726,8 @@ static cudaError_t go_part(PartParams<K> p, const PartLayout& L, char* ws, uint3
     p.res = ws + L.o_res;
     p.slot2 = (uint16_t*)(ws + L.o_slot2);
     p.b2 = (uint16_t*)(ws + L.o_b2);
-    p.thist = (uint16_t*)(ws + L.o_thist);
+    p.toff = (uint16_t*)(ws + L.o_toff);
+    p.tlim = (uint16_t*)(ws + L.o_tlim);
     p.tstart = (uint16_t*)(ws + L.o_tstart);
     p.slabcnt = (uint32_t*)(ws + L.o_slabcnt);
     p.ovf_n = (uint32_t*)(ws + L.o_ovfn);
@@ -709,7 +743,8 @@ static cudaError_t go_part(PartParams<K> p, const PartLayout& L, char* ws, uint3
     uint64_t g = 0;
     {   // partition: exactly G CTAs (tile t on CTA t % G; the unpartition relies on it)
         auto kern = k_part<K, D>;
-        const uint32_t smem = kPartTile * (uint32_t)sizeof(K) + 4u * ((1u << p.DB) + 4u * p.B + 32u) + 4u * kPartTile;
+        const uint32_t B4 = (p.B + 3u) & ~3u;
+        const uint32_t smem = kPartTile * (uint32_t)sizeof(K) + 8u * B4 + 4u * (5u * B4 + 32u) + 2u * (kPartBins + 8) + 4u * kPartTile;
         Grid grid{1u, 1u, p.G};
         e = plan_grid((const void*)kern, 1024, smem, grid, p.G, carveout_for(smem, 1024), &g, &uns);
         if (e != cudaSuccess) return e;
@@ -731,7 +766,7 @@ static cudaError_t go_part(PartParams<K> p, const PartLayout& L, char* ws, uint3
     count_launch();
     {   // back to query order (slab owner = tile % G is an address, not a CTA)
         auto kern = k_unpart<K, OB>;
-        const uint32_t smem = kPartTile * OB + 4u * (3u * p.B + 32u);
+        const uint32_t smem = kPartTile * OB + 4u * (3u * p.B);
         Grid grid{1u, 1u, sm_count};
         e = plan_grid((const void*)kern, kUnpartThreads, smem, grid, sm_count, carveout_for(smem, kUnpartThreads),
                       &g, &uns);

@@ -279,3 +279,58 @@ def test_u64_narrow_key_range(hi_log2):
         check(run(idx, q, 8, kary_mode=mode), want, q, f"mode {mode} hi={hi_log2}")
     check(run(idx, q, 8, kary_mode=7, nreg=0x34), want, q, f"pipelined hi={hi_log2}")
     idx.close()
+
+
+# ------------------------------------------------------------------ boundary (§8b error table)
+
+def test_lookup_rejects_host_pointers():
+    """bs_lookup takes device memory only (P:61 'all data GPU-resident'); a host
+    buffer is BS_ERR_INVALID, not an asynchronous fault (host buffers: bs_lookup_host)."""
+    keys = workload.gen_keys(5000, 8, seed=2)
+    q = workload.gen_queries(keys, 1000, seed=3)
+    idx = build(keys, variant=bs.KARY)
+    dq = P.as_torch(q)
+    out = torch.empty(q.size, dtype=torch.int64, device="cuda")
+    hq = torch.from_numpy(q.view(np.int64))
+    hout = torch.empty(q.size, dtype=torch.int64)
+    for a, b in ((hq, out), (dq, hout), (hq.pin_memory(), out), (dq, hout.pin_memory())):
+        with pytest.raises(bs.BsError) as e:
+            bs.bs_lookup(idx, a, q.size, b)
+        assert e.value.code == bs.BS_ERR_INVALID
+    bs.bs_lookup(idx, dq, q.size, out)          # the device path still works
+    torch.cuda.synchronize()
+    check(P.to_numpy_unsigned(out, 8), oracle.lookup(keys, q), q, "after rejections")
+    idx.close()
+
+
+def test_concurrent_lookups_on_streams():
+    """An index is immutable: lookups on one index from many streams / host
+    threads at once give the oracle's results (the launch-plan cache and the
+    shared-memory statistics are the only shared mutable state)."""
+    import threading
+    keys = workload.gen_keys(1 << 20, 8, seed=4)
+    idx = build(keys, variant=bs.KARY)
+    qs = [workload.gen_queries(keys, 1 << 18, seed=10 + i, hit_ratio=0.7) for i in range(8)]
+    dqs = [P.as_torch(q) for q in qs]
+    outs = [torch.empty(q.size, dtype=torch.int64, device="cuda") for q in qs]
+    streams = [torch.cuda.Stream() for _ in qs]
+    launches = [dict(), dict(kary_mode=6), dict(variant=bs.OPT), dict(variant=bs.NAIVE),
+                dict(reorder=bs.REORDER_SORTED), dict(kary_mode=7, nreg=0x24), dict(), dict(kary_mode=0)]
+    errs = []
+
+    def work(i):
+        try:
+            for _ in range(3):
+                bs.bs_lookup_ex(idx, dqs[i], qs[i].size, outs[i], streams[i], **launches[i])
+        except Exception as ex:   # pragma: no cover - reported below
+            errs.append(ex)
+    th = [threading.Thread(target=work, args=(i,)) for i in range(len(qs))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    torch.cuda.synchronize()
+    assert not errs, errs
+    for i, q in enumerate(qs):
+        check(P.to_numpy_unsigned(outs[i], 8), oracle.lookup(keys, q), q, f"stream {i} {launches[i]}")
+    idx.close()
