@@ -627,6 +627,17 @@ def main():
             "traffic_frac": traffic / (ms_step / 1e3) / 1e9 / peak if traffic else None,
             "traffic_key": tkey, "alg_bytes_per_launch": bpl * m, "bytes_per_lookup_alg": bpl,
             "bytes_per_lookup_model": bpl_why, "peak_source": peak_src, "per": "GPU"}
+    if bpl_why.startswith("key + out (array L2") and te and te.get("l2_read_sectors_per_lookup"):
+        # the binding roof of an L2-resident array is the L2: sectors the
+        # kernel reads (ncu) at this run's speed vs the measured random-sector L2 rate
+        lp = os.path.join(ROOT, "profiles", "l2_peak.json")
+        if os.path.exists(lp):
+            l2 = json.load(open(lp))
+            ach = te["l2_read_sectors_per_lookup"] * 32 * m / (ms_step / 1e3) / 1e9
+            pk = l2["l2_read_GBps_random_32B_sectors"]
+            roof["l2"] = {"bound": "l2", "achieved": ach, "peak": pk, "unit": "GB/s", "frac": ach / pk,
+                          "sectors_per_lookup": te["l2_read_sectors_per_lookup"],
+                          "peak_source": "measured (profiles/l2_peak.json, random 32-B sectors from an L2-resident buffer)"}
     if te and te.get("kernels"):
         # a step of several kernels: the roofline is the step's (sum of its launches); shares beside it
         roof["kernels"] = [{"kernel": k["kernel"], "share_ncu": k["ms"] / te["ncu_ms"],

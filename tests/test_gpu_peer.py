@@ -4,7 +4,8 @@ SURVEY §8f f1): bit-exact vs the oracle on the concatenated array.
 * world = 1: the route kernel stores every query into the rank's own window,
   the K-ary kernel's peer epilogue stores every result into its own return
   window; consecutive calls exercise the monotonic counters.
-* world = 2 on ONE GPU: two processes, each with its own window, mapped into
+* world = 2 (one process per GPU; skipped on a one-GPU box — round 1 ran it as two processes on ONE GPU,
+  which B200_PROFILING.md forbids): each process has its own window, mapped into
   the other with CUDA IPC — the same code path as two GPUs over NVLink, with a
   run of duplicates straddling the shard boundary (first-occurrence routing).
 """
@@ -105,7 +106,7 @@ def _world2_worker(rank, world, port, keys, cut, calls, ret, kb=8):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    torch.cuda.set_device(0)
+    torch.cuda.set_device(rank)   # one process per GPU (ranks that wait on each other must not share one)
     shard = keys[:cut] if rank == 0 else keys[cut:]
     max_m = max(m for m, _ in calls)
     idx = bs.bs_build_peer(P.as_torch(shard), shard.size, _layout(kb), rank, world, max_m)
@@ -127,7 +128,13 @@ def _world2_worker(rank, world, port, keys, cut, calls, ret, kb=8):
 
 @pytest.mark.timeout(600)
 @pytest.mark.parametrize("kb", [8, 4])
-def test_peer_world2_one_gpu(kb):
+def test_peer_world2(kb):
+    """World 2, one process per GPU.  Needs two GPUs: B200_PROFILING.md forbids
+    running ranks whose kernels wait on each other as processes on ONE GPU
+    (Xid 109 seen with 2-4 such ranks), which round 1 did; the rank logic is
+    also covered on CPU (tests/test_dist_cpu.py, tests/test_bench_cpu.py)."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs: peer ranks that wait on each other must not share a GPU")
     import torch.multiprocessing as mp
     keys = workload.gen_keys(300000, kb, seed=31)
     cut = 150000
