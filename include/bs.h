@@ -66,11 +66,20 @@ typedef enum {
                               batch there.  Any variant's index.  Correct for ANY batch order
                               (queries outside their segment's range take a global
                               bisection); fast only when the batch is ascending.             */
-    BS_REORDER_GLOBAL = 4  /* the batch is reordered GLOBALLY (the paper's out-of-place reference
+    BS_REORDER_GLOBAL = 4, /* the batch is reordered GLOBALLY (the paper's out-of-place reference
                               point): one partition pass groups the queries by the
                               8192-key segment that holds their answer (records in a caller
                               workspace), the segment-staged lookup runs per segment, one pass
                               restores query order.  Needs bs_lookup_ws; n <= 2^26 keys.     */
+    BS_REORDER_BUCKET = 5  /* the batch is partitioned by KEY RANGE (P:131-135's global reorder made
+                              coarse): buckets of 2^15 leaves of 32 B (2^17 u64 / 2^18 u32 keys,
+                              an L2-sized slice of the array); one histogram pass, one partition
+                              pass (bucket-major, exact offsets), the per-bucket search (the
+                              bucket's pinned Eytzinger table of leaf maxima staged in shared
+                              memory by TMA, §4.2, then one 32-B leaf, §5), one pass restoring
+                              query order.  Any variant's index (bs_build always builds the
+                              bucket tables, n * key_bytes / 8 bytes, up to 4096 buckets:
+                              n <= 2^29 u64 / 2^30 u32 keys).  Needs bs_lookup_ws.             */
 } bs_reorder;
 
 /* Build-time structure + default launch configuration.
@@ -91,7 +100,8 @@ typedef struct {
                                kept in shared memory (§5.1); 0 = no pinning;
                                0xFFFFFFFF = largest that fits                              */
     uint32_t pin_partial;   /* OPT: 1 = "full-pinning" (partial step M+1), 0 = "steps-pinning" */
-    uint32_t reorder;       /* bs_reorder: 1-2 OPT only; 3 (SORTED), 4 (GLOBAL) any variant */
+    uint32_t reorder;       /* bs_reorder: 1-2 OPT only; 3 (SORTED), 4 (GLOBAL), 5 (BUCKET) any
+                               variant                                                      */
     uint32_t k;             /* KARY fan-out K, 2..33 (P:223 A6000 best K = 17)       */
     uint32_t leaf_chunk;    /* KARY leaf chunk C in keys, power of two 1..256; 0 =
                                auto (layout default), resolved by bs_build: the smallest
@@ -252,17 +262,18 @@ int bs_lookup_host(const void* idx, const void* host_queries, uint64_t m, void* 
                    void* stream);
 
 /*
- * Workspace-taking lookup (the BS_REORDER_GLOBAL mode, which partitions the
- * batch out of place).
+ * Workspace-taking lookup (the BS_REORDER_GLOBAL and BS_REORDER_BUCKET modes,
+ * which partition the batch out of place).
  *   bs_workspace_bytes: *bytes = device bytes a bs_lookup_ws call with this
  *     launch (NULL = index defaults) needs for m queries (0 if the mode needs
- *     none).  BS_ERR_UNSUPPORTED if the mode cannot run on this index (GLOBAL:
- *     n > 2^26 keys, or m >= 2^32).
+ *     none; BUCKET: m * (key + out + 4) bytes plus per-CTA / per-tile tables).
+ *     BS_ERR_UNSUPPORTED if the mode cannot run on this index (GLOBAL:
+ *     n > 2^26 keys; BUCKET: more than 4096 buckets; either: m >= 2^32).
  *   bs_lookup_ws: bs_lookup_ex plus a caller-owned device workspace `ws` of
  *     ws_bytes (no allocation inside; the workspace must not be shared by calls
  *     in flight on other streams).  BS_ERR_INVALID if ws is NULL / too small for
  *     a mode that needs one.  Other modes ignore ws.  Same result contract.
- * bs_lookup / bs_lookup_ex with reorder = BS_REORDER_GLOBAL return
+ * bs_lookup / bs_lookup_ex with reorder = BS_REORDER_GLOBAL or BUCKET return
  * BS_ERR_INVALID (no workspace).
  */
 int bs_workspace_bytes(const void* idx, uint64_t m, const bs_launch* launch, uint64_t* bytes);

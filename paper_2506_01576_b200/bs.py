@@ -24,7 +24,7 @@ HEADER = os.path.join(os.path.dirname(_HERE), "include", "bs.h")
 BS_OK, BS_ERR_INVALID, BS_ERR_UNSUPPORTED, BS_ERR_OOM, BS_ERR_CUDA, BS_ERR_NCCL, BS_ERR_NOT_SORTED = 0, -1, -2, -3, -4, -5, -6
 NAIVE, OPT, KARY = 0, 1, 2
 DYNAMIC, STATIC = 0, 1
-REORDER_NONE, REORDER_LOOKUP, REORDER_FULL, REORDER_SORTED, REORDER_GLOBAL = 0, 1, 2, 3, 4
+REORDER_NONE, REORDER_LOOKUP, REORDER_FULL, REORDER_SORTED, REORDER_GLOBAL, REORDER_BUCKET = 0, 1, 2, 3, 4, 5
 HINT_STREAM_EVICT_FIRST, HINT_LEAF_EVICT_FIRST, HINT_SEP_EVICT_LAST = 1, 2, 4
 EXPORT_SORTED, EXPORT_PINNED, EXPORT_KARY = 0, 1, 2
 DIST_REPLICATED, DIST_PARTITIONED = 0, 1

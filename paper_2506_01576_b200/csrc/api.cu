@@ -2,6 +2,7 @@
 // build orchestration and variant dispatch.  Host code only; the kernels live
 // in naive.cu / opt.cu / kary.cu / build.cu.
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <atomic>
@@ -112,6 +113,8 @@ cudaError_t plan_grid(const void* kern, uint32_t threads, uint32_t smem, Grid gr
     return cudaSuccess;
 }
 
+static uint64_t bucket_max_keys(uint32_t kb) { return (uint64_t)kBkMaxBuckets << 15 << (kb == 8 ? 2 : 3); }
+
 static bool is_pow2(uint64_t x) { return x && !(x & (x - 1)); }
 
 static uint32_t pow2_at_least(uint32_t x) {
@@ -132,6 +135,7 @@ static void free_index(Index* ix) {
     if (ix->d_flat) cudaFree(ix->d_flat);
     if (ix->d_flat64) cudaFree(ix->d_flat64);
     if (ix->d_flatimg) cudaFree(ix->d_flatimg);
+    if (ix->d_bk) cudaFree(ix->d_bk);
     destroy_host_ctx(ix);
     destroy_dist_state(ix);
     destroy_peer_state(ix);
@@ -380,6 +384,44 @@ const char* bs_version(void) {
     return "libbs 0.1 (sm_100a; naive / opt / kary; arXiv 2506.01576)";
 }
 
+// Buckets of 2^D leaves of 32 B (D = 15; BS_BUCKET_D = 14 for A/B runs): the
+// tables, per-bucket image parameters, bucket maxima and their directory in one
+// allocation.  Not built (the mode reports UNSUPPORTED) above kBkMaxBuckets.
+static int build_bucket_layout(Index* ix, cudaStream_t st, BuildTimer& bt) {
+    uint32_t D = 15;
+    if (const char* v = getenv("BS_BUCKET_D")) D = (uint32_t)atoi(v) == 14 ? 14u : 15u;
+    const uint64_t NB = (1ull << D) * (32u / ix->kb);
+    const uint64_t B = (ix->n + NB - 1) / NB;
+    if (B > kBkMaxBuckets) return BS_OK;
+    cudaError_t e = cudaStreamSynchronize(st);   // a_first / a_last are on the host
+    if (e != cudaSuccess) return fail_cuda(e, "bucket tables: sync");
+    auto al = [](uint64_t x) { return (x + 255) & ~255ull; };
+    const uint64_t o_tab = 0, o_par = al(4 * (B << D)), o_mx = o_par + al(16 * B), o_dir = o_mx + al(4 * B);
+    const uint64_t total = o_dir + al(2 * ((1u << 13) + 1));
+    e = cudaMalloc(&ix->d_bk, total);
+    if (e != cudaSuccess) return fail_cuda(e, "cudaMalloc(bucket tables)");
+    BucketIndex& bi = ix->bk;
+    char* p = (char*)ix->d_bk;
+    bi.B = B;
+    bi.D = D;
+    bi.gbase = ix->a_first;
+    const uint64_t span = ix->a_last - ix->a_first;
+    uint32_t bl = 0;
+    while (bl < 64 && (span >> bl) != 0) ++bl;
+    bi.gsh = bl > 32 ? bl - 32 : 0;
+    bt.begin(kStImg);
+    e = build_bucket_index(ix->kb, ix->d_keys, ix->n, D, B, bi.gbase, bi.gsh, (uint32_t*)(p + o_tab),
+                           (uint64_t*)(p + o_par), (uint32_t*)(p + o_mx), (uint16_t*)(p + o_dir), st);
+    bt.end();
+    if (e != cudaSuccess) return fail_cuda(e, "build_bucket_index");
+    bi.tab = (const uint32_t*)(p + o_tab);
+    bi.par = (const uint64_t*)(p + o_par);
+    bi.mx = (const uint32_t*)(p + o_mx);
+    bi.dir = (const uint16_t*)(p + o_dir);
+    ix->bk_bytes = total;
+    return BS_OK;
+}
+
 int bs_layout_default(bs_layout* l) {
     if (!l) return fail(BS_ERR_INVALID, "bs_layout_default: NULL");
     memset(l, 0, sizeof *l);
@@ -420,7 +462,7 @@ int bs_build(const void* keys, uint64_t n, const bs_layout* layout_in, void** ou
     if (lay.out_bytes == 4 && n >= (1ull << 31)) return fail(BS_ERR_INVALID, "out_bytes = 4 requires n < 2^31");
     if (lay.variant > BS_VARIANT_KARY) return fail(BS_ERR_INVALID, "unknown variant %u", lay.variant);
     if (lay.schedule > BS_SCHED_STATIC) return fail(BS_ERR_INVALID, "unknown schedule %u", lay.schedule);
-    if (lay.reorder > BS_REORDER_GLOBAL) return fail(BS_ERR_INVALID, "unknown reorder %u", lay.reorder);
+    if (lay.reorder > BS_REORDER_BUCKET) return fail(BS_ERR_INVALID, "unknown reorder %u", lay.reorder);
     if (lay.kary_mode > BS_KARY_MODE_AUTO) return fail(BS_ERR_INVALID, "unknown kary_mode %u", lay.kary_mode);
     if (lay.k < 2 || lay.k > 33) return fail(BS_ERR_INVALID, "K must be in [2, 33]");
     if (lay.leaf_chunk != 0 && (!is_pow2(lay.leaf_chunk) || lay.leaf_chunk > 256))
@@ -571,6 +613,10 @@ int bs_build(const void* keys, uint64_t n, const bs_layout* layout_in, void** ou
         ix->kary_built = true;
     }
 
+    // ---- per-bucket pinned tables for BS_REORDER_BUCKET (part.cu) ----
+    rc = build_bucket_layout(ix, st, bt);
+    if (rc != BS_OK) goto done;
+
     cudaEventRecord(e1, st);
     e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) { rc = fail_cuda(e, "bs_build sync"); goto done; }
@@ -623,7 +669,7 @@ static int lookup_impl(const void* idx, const void* queries, uint64_t m, void* o
         bs_launch_default(idx, &L);
     }
     if (L.kary_mode > 7) return fail(BS_ERR_INVALID, "bs_lookup: unknown kary_mode %u", L.kary_mode);
-    if (L.reorder > BS_REORDER_GLOBAL) return fail(BS_ERR_INVALID, "bs_lookup: unknown reorder %u", L.reorder);
+    if (L.reorder > BS_REORDER_BUCKET) return fail(BS_ERR_INVALID, "bs_lookup: unknown reorder %u", L.reorder);
     if (m == 0) return BS_OK;
     if (!queries || !out) return fail(BS_ERR_INVALID, "bs_lookup: NULL queries/out with m > 0");
     const uintptr_t q0 = (uintptr_t)queries, q1 = q0 + m * ix->kb;
@@ -650,6 +696,26 @@ static int lookup_impl(const void* idx, const void* queries, uint64_t m, void* o
         if (e != cudaSuccess) return fail_cuda(e, "global partition launch");
         return BS_OK;
     }
+    if (L.reorder == BS_REORDER_BUCKET) {
+        uint64_t need = 0;
+        if (!ix->bk.tab || !bucket_workspace_bytes(ix->bk.B, m, ix->kb, ix->ob, (uint32_t)ix->sm_count, &need))
+            return fail(BS_ERR_UNSUPPORTED, "BS_REORDER_BUCKET: needs n <= %llu keys and m < 2^32",
+                        (unsigned long long)bucket_max_keys(ix->kb));
+        if (!ws) return fail(BS_ERR_INVALID, "BS_REORDER_BUCKET needs a workspace: bs_lookup_ws");
+        if (ws_bytes < need)
+            return fail(BS_ERR_INVALID, "bs_lookup_ws: workspace of %llu B < %llu B", (unsigned long long)ws_bytes,
+                        (unsigned long long)need);
+        if (!device_accessible(ws, ix->device)) return fail(BS_ERR_INVALID, "bs_lookup_ws: ws must be device memory");
+        bool uns = false;
+        uint32_t chunk = 0;
+        if (const char* v = getenv("BS_BUCKET_CHUNK")) chunk = (uint32_t)atoi(v);
+        cudaError_t e = launch_bucket(ix->kb, ix->ob, ix->bk, ix->d_keys, ix->n, queries, m, out,
+                                      (L.cache_hints & BS_HINT_STREAM_EVICT_FIRST) ? 1u : 0u, chunk, ws, ws_bytes,
+                                      (uint32_t)ix->sm_count, (cudaStream_t)stream, &uns);
+        if (uns) return fail(BS_ERR_UNSUPPORTED, "BS_REORDER_BUCKET: not supported for this index / batch");
+        if (e != cudaSuccess) return fail_cuda(e, "bucket partition launch");
+        return BS_OK;
+    }
     return dispatch_lookup(ix, queries, m, out, (cudaStream_t)stream, L);
 }
 
@@ -673,6 +739,12 @@ int bs_workspace_bytes(const void* idx, uint64_t m, const bs_launch* launch, uin
         bs_launch_default(idx, &L);
     }
     *bytes = 0;
+    if (L.reorder == BS_REORDER_BUCKET) {
+        if (!ix->bk.tab || !bucket_workspace_bytes(ix->bk.B, m, ix->kb, ix->ob, (uint32_t)ix->sm_count, bytes))
+            return fail(BS_ERR_UNSUPPORTED, "BS_REORDER_BUCKET: needs n <= %llu keys and m < 2^32",
+                        (unsigned long long)bucket_max_keys(ix->kb));
+        return BS_OK;
+    }
     if (L.reorder != BS_REORDER_GLOBAL) return BS_OK;
     if (!part_workspace_bytes(ix->n, m, ix->kb, ix->ob, (uint32_t)ix->sm_count, bytes))
         return fail(BS_ERR_UNSUPPORTED, "BS_REORDER_GLOBAL: needs n <= 2^26 keys and m < 2^32");
@@ -711,6 +783,7 @@ int bs_index_info(const void* idx, bs_info* info) {
     if (ix->d_img64) info->footprint_bytes += (uint64_t)ix->img64_base[ix->img64_L] * 8;
     if (ix->d_flat) info->footprint_bytes += (1ull << ix->flat_D) * (ix->d_flat64 ? 12 : 4);
     if (ix->d_flatimg) info->footprint_bytes += ((1ull << ix->flat_D) + ix->flat_img_words) * 4;
+    info->footprint_bytes += ix->bk_bytes;
     info->build_ms = ix->build_ms;
     for (int i = 0; i < 5; ++i) info->build_stage_us[i] = (uint32_t)(ix->build_stage_ms[i] * 1000.0f + 0.5f);
     info->sm_count = ix->sm_count;

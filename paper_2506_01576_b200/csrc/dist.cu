@@ -343,7 +343,7 @@ int bs_lookup_dist(const void* idx, const void* local_queries, uint64_t m_local,
     if (racc) {
         bs_launch Ld;
         bs_launch_default(idx, &Ld);
-        if (Ld.reorder == BS_REORDER_GLOBAL) Ld.reorder = BS_REORDER_NONE;   // no workspace here
+        if (Ld.reorder == BS_REORDER_GLOBAL || Ld.reorder == BS_REORDER_BUCKET) Ld.reorder = BS_REORDER_NONE;   // no workspace here
         int rc = bs_lookup_ex(idx, d->d_recvq, racc, d->d_recvres, s, &Ld);
         if (rc != BS_OK) return rc;
         k_add_base<<<grid_of(racc), 256, 0, s>>>(d->d_recvres, racc, d->base[me]);

@@ -93,9 +93,9 @@ extern "C" int bs_lookup_host(const void* idx, const void* host_q, uint64_t m, v
     HostCtx* h = ix->host;
     bs_launch L;
     bs_launch_default(idx, &L);
-    // chunks are looked up in the index's default mode; the out-of-place GLOBAL
-    // reordering needs a caller workspace, so chunks take the in-place path
-    if (L.reorder == BS_REORDER_GLOBAL) L.reorder = BS_REORDER_NONE;
+    // chunks are looked up in the index's default mode; the out-of-place GLOBAL /
+    // BUCKET reorderings need a caller workspace, so chunks take the in-place path
+    if (L.reorder == BS_REORDER_GLOBAL || L.reorder == BS_REORDER_BUCKET) L.reorder = BS_REORDER_NONE;
     const bool pin_q = is_pinned(host_q), pin_o = is_pinned(host_out);
     const uint32_t kb = ix->kb, ob = ix->ob;
 

@@ -90,6 +90,11 @@ struct Index {
     uint64_t flat_fbase = 0;
     uint32_t flat_fshift = 32;
 
+    // BS_REORDER_BUCKET: per-bucket pinned tables (part.cu); bk.tab == nullptr: not built
+    BucketIndex bk;
+    void* d_bk = nullptr;            // one allocation: tab | par | mx | dir
+    uint64_t bk_bytes = 0;
+
     // device
     int sm_count = 148, smem_optin = 232448, smem_per_sm = 233472, l2_bytes = 0;
     double build_ms = 0;

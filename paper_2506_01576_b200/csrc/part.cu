@@ -1,0 +1,764 @@
+// part.cu — BS_REORDER_BUCKET: a random batch turned into L2-local work.
+//
+// PAPER.md §4.3: neighbouring lookups in key order share their
+// search paths; the paper sorts lookups locally (per thread block) because a
+// global, out-of-place sort of the batch is "too expensive".  On B200 the
+// random-order lookup is bound by one random DRAM line per lookup (the DRAM
+// atom), so the only way past ~36 G random lines/s is to make
+// the array accesses of a batch local in time.  This mode partitions the batch
+// by KEY RANGE into buckets whose slice of the array fits L2, searches bucket
+// after bucket, and restores query order — a coarse global reorder that costs
+// three streaming passes instead of a sort:
+//
+//   k_bk_hist    per CTA: histogram of its tiles' queries over the B buckets
+//   k_bk_scan    per bucket: exclusive prefix of the CTA histograms
+//   k_bk_part    per tile of T queries: bucket each query, counting-sort the tile
+//                by bucket in shared memory, append each bucket's run to the
+//                CTA's slice of that bucket's region (bucket-major, exact
+//                offsets: no atomics in global memory, no overflow), and record
+//                for every sorted position its bucket and original slot
+//   k_bk_search  items of CH queries in bucket order: per bucket, a pinned
+//                Eytzinger table of its 2^D leaf maxima (§4.2's pinned top
+//                levels of a binary search, built by bs_build) is staged once by
+//                TMA; each lookup descends D levels in shared memory, reads its
+//                32-B leaf (one sector, L2-resident while the bucket is worked
+//                on) and counts the keys < q (§5's leaf scan)
+//   k_bk_unpart  per tile: gather the results of its runs, scatter them to query
+//                order in shared memory, one coalesced store (Listing 2 l.35-39's
+//                "unsort", at batch scale)
+//
+// Bucket b covers the array positions [b*NB, (b+1)*NB), NB = 2^D leaves of LK
+// keys (LK = 32 B / key); a query belongs to bucket #(bucket maxima < q) (the
+// last bucket also takes the queries above every key).  The bucket is exact, so
+// the per-bucket search never leaves its bucket.
+#include <cstdlib>
+#include <cstring>
+#include <type_traits>
+
+#include "common.cuh"
+#include "params.h"
+
+namespace bs {
+
+constexpr uint32_t kBkTile = 4096;        // queries per partition tile (u16 slots)
+constexpr uint32_t kBkPThreads = 512;     // threads of the streaming passes (hist / part / unpart)
+constexpr uint32_t kBkBinsLog2 = 13;      // radix directory over the 32-bit global image
+constexpr uint32_t kBkBins = 1u << kBkBinsLog2;
+constexpr uint32_t kBkThreads = 1024;        // threads of the search (one CTA per SM)
+
+// order-preserving 32-bit image of x over [base, ...): 0 at or below base,
+// (x - base) >> sh clamped to 2^32 - 1 (exact when the span fits 32 bits)
+__device__ __forceinline__ uint32_t bk_img(uint64_t x, uint64_t base, uint32_t sh) {
+    if (x <= base) return 0u;
+    const uint64_t d = (x - base) >> sh;
+    return d > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)d;
+}
+
+// shift that makes a span fit 32 bits
+__host__ __device__ __forceinline__ uint32_t bk_shift(uint64_t span) {
+    uint32_t bl = 0;
+    while (bl < 64 && (span >> bl) != 0) ++bl;
+    return bl > 32u ? bl - 32u : 0u;
+}
+
+// 32 bytes of keys (one sector) without L1 allocation, with an L2 policy
+__device__ __forceinline__ void ld_sector(const void* p, uint64_t pol, uint64_t* x) {
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u64 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=l"(x[0]), "=l"(x[1]), "=l"(x[2]), "=l"(x[3]) : "l"(p), "l"(pol));
+}
+
+template <class K>
+__device__ __forceinline__ K bk_key(const uint64_t* x, int u) {
+    if constexpr (sizeof(K) == 8) return x[u];
+    else return (uint32_t)(x[u >> 1] >> (32 * (u & 1)));
+}
+
+// ------------------------------------------------------------------ build
+
+// Per bucket b: the Eytzinger table of its leaf maxima images (slot s >= 1
+// holds in-order leaf i = (2j+1) 2^(D-1-d) - 1 for s = 2^d + j; slot 0 unused;
+// leaves past the array: 0xFFFFFFFF) and its image parameters (base, shift).
+template <class K>
+__global__ void k_bk_build_tab(const K* __restrict__ a, uint64_t n, uint32_t D, uint32_t LK, uint64_t B,
+                               uint32_t* __restrict__ tab, uint64_t* __restrict__ par) {
+    const uint64_t S = 1ull << D, NB = S * LK;
+    const uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= B * S) return;
+    const uint64_t b = g >> D, s = g & (S - 1);
+    const uint64_t lo = b * NB, len = (n - lo) < NB ? (n - lo) : NB;
+    const uint64_t base = (uint64_t)a[lo];
+    const uint32_t sh = bk_shift((uint64_t)a[lo + len - 1] - base);
+    if (s == 0) {
+        par[2 * b] = base;
+        par[2 * b + 1] = sh;
+        tab[g] = 0;
+        return;
+    }
+    const uint32_t d = 31u - (uint32_t)__clz((int)(uint32_t)s);
+    const uint64_t j = s - (1ull << d);
+    const uint64_t i = (2 * j + 1) * (1ull << (D - 1 - d)) - 1;   // in-order leaf
+    const uint64_t Mb = (len + LK - 1) / LK;
+    uint32_t f = 0xFFFFFFFFu;
+    if (i < Mb) {
+        const uint64_t e = (i + 1) * LK < len ? (i + 1) * LK : len;
+        f = bk_img((uint64_t)a[lo + e - 1], base, sh);
+    }
+    tab[g] = f;
+}
+
+// Global images of the bucket maxima (b < B-1; [B-1] = 0xFFFFFFFF) and the
+// radix directory dir[x] = #(b < B-1 : max image < x << (32 - kBkBinsLog2)).
+template <class K>
+__global__ void k_bk_build_dir(const K* __restrict__ a, uint64_t n, uint64_t NB, uint32_t B, uint64_t gbase,
+                               uint32_t gsh, uint32_t* __restrict__ mx, uint16_t* __restrict__ dir) {
+    const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g < B) mx[g] = g + 1 < B ? bk_img((uint64_t)a[((uint64_t)g + 1) * NB - 1], gbase, gsh) : 0xFFFFFFFFu;
+    if (g <= kBkBins) {
+        const uint64_t f = (uint64_t)g << (32 - kBkBinsLog2);
+        uint32_t lo = 0, hi = B - 1;
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            const uint64_t v = bk_img((uint64_t)a[((uint64_t)mid + 1) * NB - 1], gbase, gsh);
+            if (v < f) lo = mid + 1;
+            else hi = mid;
+        }
+        dir[g] = (uint16_t)lo;
+    }
+}
+
+cudaError_t build_bucket_index(int kb, const void* a, uint64_t n, uint32_t D, uint64_t B, uint64_t gbase,
+                               uint32_t gsh, uint32_t* tab, uint64_t* par, uint32_t* mx, uint16_t* dir,
+                               cudaStream_t s) {
+    const uint32_t LK = 32u / (uint32_t)kb;
+    const uint64_t NB = (1ull << D) * LK;
+    const uint64_t tot = B << D;
+    const uint32_t g1 = (uint32_t)((tot + 255) / 256);
+    const uint32_t g2 = (uint32_t)(((B > kBkBins + 1 ? B : kBkBins + 1) + 255) / 256);
+    if (kb == 8) {
+        k_bk_build_tab<uint64_t><<<g1, 256, 0, s>>>((const uint64_t*)a, n, D, LK, B, tab, par);
+        k_bk_build_dir<uint64_t><<<g2, 256, 0, s>>>((const uint64_t*)a, n, NB, (uint32_t)B, gbase, gsh, mx, dir);
+    } else {
+        k_bk_build_tab<uint32_t><<<g1, 256, 0, s>>>((const uint32_t*)a, n, D, LK, B, tab, par);
+        k_bk_build_dir<uint32_t><<<g2, 256, 0, s>>>((const uint32_t*)a, n, NB, (uint32_t)B, gbase, gsh, mx, dir);
+    }
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ lookup
+
+template <class K>
+struct BkParams {
+    const K* a;
+    uint64_t n;
+    const K* q;
+    uint64_t m;
+    void* out;
+    uint32_t B;              // buckets
+    uint32_t D;              // per-bucket table depth: 2^D leaves of LK keys per bucket
+    uint64_t NB;             // keys per bucket = 2^D * LK
+    const uint32_t* tab;     // [B << D] per-bucket Eytzinger tables
+    const uint64_t* par;     // [2B] per-bucket image base, shift
+    const uint32_t* mx;      // [B] global images of the bucket maxima
+    const uint16_t* dir;     // [kBkBins + 1] radix directory over mx
+    uint64_t gbase;          // global image: bk_img(x, gbase, gsh)
+    uint32_t gsh;
+    uint32_t G;              // CTAs of hist / part / unpart (tile t on CTA t % G)
+    uint32_t Gs;             // CTAs of the search (one per SM)
+    uint32_t CH;             // queries per search item
+    uint32_t stream_hint;
+    // workspace
+    uint32_t* cnt;           // [G * B] per-CTA bucket counts -> exclusive prefix within the bucket
+    uint32_t* tot;           // [B] bucket sizes
+    K* rq;                   // [m] queries, bucket-major
+    void* rp;                // [m] their results, same positions
+    uint32_t* bp;            // [m] tile t's sorted position s: bucket | original slot << 16
+    uint32_t* trun;          // [ntiles * B] (global position of run b) - (its sorted start), mod 2^32
+};
+
+// bucket of x: #(bucket maxima < x).  The radix directory packs, per bin of
+// the 32-bit global image, the candidate bucket range [lo, hi] (lo | hi << 16):
+// #(maxima images < x's image) lies in it.  With more bins than buckets a bin
+// holds at most one maximum almost always, so one predicated compare settles
+// it; a bin with more maxima continues by bisection, and maxima whose image
+// ties x's are compared exactly (galloping over the real maxima a[(j+1) NB - 1]).
+template <class K>
+__device__ __forceinline__ uint32_t bk_bucket(const BkParams<K>& p, const uint32_t* MS, const uint32_t* DIR, K x) {
+    const uint32_t fx = bk_img((uint64_t)x, p.gbase, p.gsh);
+    const uint32_t w = DIR[fx >> (32 - kBkBinsLog2)];
+    uint32_t l = w & 0xFFFFu, h = w >> 16;
+    bool more = false, tie = false;
+    if (l < h) {
+        const uint32_t v = MS[l];
+        const bool lt = v < fx;
+        tie = v == fx;
+        l += lt ? 1u : 0u;
+        more = lt && l < h;   // a second maximum in the bin, and x above the first
+    }
+    if (__builtin_expect(more || tie, 0)) {
+        // rare: more maxima in the bin, or an image tie
+        while (l < h) {
+            const uint32_t mid = (l + h) >> 1;
+            if (MS[mid] < fx) l = mid + 1;
+            else h = mid;
+        }
+        const uint32_t nm = p.B - 1;
+        auto mxv = [&](uint32_t j) -> K { return ldg(p.a + ((uint64_t)j + 1) * p.NB - 1); };
+        if (l < nm && MS[l] == fx && mxv(l) < x) {
+            // step over the maxima that share x's image and are still < x: gallop, then bisect
+            uint32_t lo = l + 1, step = 1, hi;
+            for (;;) {
+                hi = lo - 1 + step;
+                if (hi >= nm) { hi = nm; break; }
+                if (mxv(hi) >= x) break;
+                lo = hi + 1;
+                step <<= 1;
+            }
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (mxv(mid) < x) lo = mid + 1;
+                else hi = mid;
+            }
+            l = lo;
+        }
+    }
+    return l;
+}
+
+// stage the bucket maxima images and the packed directory (plain loads; once per CTA)
+template <class K>
+__device__ __forceinline__ void bk_stage_dir(const BkParams<K>& p, uint32_t* MS, uint32_t* DIR) {
+    for (uint32_t i = threadIdx.x; i < p.B; i += blockDim.x) MS[i] = p.mx[i];
+    for (uint32_t i = threadIdx.x; i < kBkBins; i += blockDim.x) DIR[i] = (uint32_t)p.dir[i] | ((uint32_t)p.dir[i + 1] << 16);
+}
+
+// block-wide exclusive scan of v[0..N) in place (blockDim.x = 1024); returns the total
+__device__ __forceinline__ uint32_t bk_exscan(uint32_t* v, uint32_t N, uint32_t* tmp) {
+    const uint32_t per = (N + blockDim.x - 1) / blockDim.x;
+    const uint32_t b0 = threadIdx.x * per;
+    uint32_t s = 0;
+    for (uint32_t i = 0; i < per; ++i)
+        if (b0 + i < N) s += v[b0 + i];
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t inc = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+        if (lane >= (uint32_t)o) inc += y;
+    }
+    if (lane == 31) tmp[w] = inc;
+    __syncthreads();
+    if (w == 0) {
+        const uint32_t x = lane < (blockDim.x >> 5) ? tmp[lane] : 0u;
+        uint32_t wi = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, wi, o);
+            if (lane >= (uint32_t)o) wi += y;
+        }
+        tmp[lane] = wi - x;
+        if (lane == 31) tmp[32] = wi;
+    }
+    __syncthreads();
+    uint32_t run = tmp[w] + inc - s;
+    for (uint32_t i = 0; i < per; ++i) {
+        if (b0 + i < N) {
+            const uint32_t c = v[b0 + i];
+            v[b0 + i] = run;
+            run += c;
+        }
+    }
+    const uint32_t total = tmp[32];
+    __syncthreads();
+    return total;
+}
+
+// ---- pass 1: per-CTA histograms (same tile -> CTA map as k_bk_part); the next
+// tile's queries are in flight while this tile is bucketed
+template <class K>
+__global__ void __launch_bounds__(kBkPThreads, 2)
+k_bk_hist(const BkParams<K> p) {
+    constexpr uint32_t T = kBkTile, E = T / kBkPThreads;
+    extern __shared__ __align__(16) uint32_t sm[];
+    const uint32_t B4 = (p.B + 3u) & ~3u;
+    uint32_t* MS = sm;
+    uint32_t* hist = MS + B4;
+    uint32_t* DIR = hist + B4;                                // [kBkBins]
+    bk_stage_dir(p, MS, DIR);
+    for (uint32_t b = threadIdx.x; b < p.B; b += blockDim.x) hist[b] = 0;
+    __syncthreads();
+    const uint64_t pol = p.stream_hint ? policy_evict_first() : policy_evict_normal();
+    const uint64_t ntiles = (p.m + T - 1) / T;
+    auto load_tile = [&](uint64_t t, K* xs) {
+        const uint64_t b0 = t * T;
+#pragma unroll
+        for (uint32_t e = 0; e < E; ++e) {
+            const uint64_t j = b0 + e * kBkPThreads + threadIdx.x;
+            xs[e] = (t < ntiles && j < p.m) ? load_stream(p.q + j, true, pol) : (K)0;
+        }
+    };
+    K xn[E];
+    load_tile(blockIdx.x, xn);
+    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const uint64_t b0 = t * T;
+        const uint32_t cntq = (uint32_t)((p.m - b0) < T ? (p.m - b0) : T);
+        K x[E];
+#pragma unroll
+        for (uint32_t e = 0; e < E; ++e) x[e] = xn[e];
+        load_tile(t + gridDim.x, xn);
+#pragma unroll
+        for (uint32_t e = 0; e < E; ++e)
+            if (e * kBkPThreads + threadIdx.x < cntq) atomicAdd(&hist[bk_bucket(p, MS, DIR, x[e])], 1u);
+    }
+    __syncthreads();
+    for (uint32_t b = threadIdx.x; b < p.B; b += blockDim.x) p.cnt[(uint64_t)blockIdx.x * p.B + b] = hist[b];
+}
+
+// ---- pass 2: per bucket, the exclusive prefix of the G CTA counts (32 buckets per CTA)
+__global__ void __launch_bounds__(1024)
+k_bk_scan(uint32_t* __restrict__ cnt, uint32_t* __restrict__ tot, uint32_t G, uint32_t B) {
+    __shared__ uint32_t part[32][33];
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint32_t b = blockIdx.x * 32 + lane;
+    const uint32_t c0 = G * w / 32, c1 = G * (w + 1) / 32;
+    uint32_t s = 0;
+    if (b < B)
+        for (uint32_t c = c0; c < c1; ++c) s += cnt[(uint64_t)c * B + b];
+    part[w][lane] = s;
+    __syncthreads();
+    if (w == 0) {
+        uint32_t run = 0;
+        for (uint32_t i = 0; i < 32; ++i) {
+            const uint32_t v = part[i][lane];
+            part[i][lane] = run;
+            run += v;
+        }
+        if (b < B) tot[b] = run;
+    }
+    __syncthreads();
+    if (b < B) {
+        uint32_t run = part[w][lane];
+        for (uint32_t c = c0; c < c1; ++c) {
+            const uint64_t o = (uint64_t)c * B + b;
+            const uint32_t v = cnt[o];
+            cnt[o] = run;
+            run += v;
+        }
+    }
+}
+
+// ---- pass 3: partition (tile t on CTA t % G, as in k_bk_hist)
+template <class K>
+__global__ void __launch_bounds__(kBkPThreads, 2)
+k_bk_part(const BkParams<K> p) {
+    constexpr uint32_t T = kBkTile, E = T / kBkPThreads;
+    extern __shared__ __align__(16) uint32_t sm[];
+    const uint32_t B = p.B, B4 = (B + 3u) & ~3u;
+    K* stq = reinterpret_cast<K*>(sm);                        // [T] queries, bucket order
+    uint32_t* sbp = reinterpret_cast<uint32_t*>(stq + T);     // [T] bucket | original slot << 16, bucket order
+    uint32_t* MS = sbp + T;                                   // [B4]
+    uint32_t* hist = MS + B4;                                 // [B4] tile counts
+    uint32_t* loff = hist + B4;                               // [B4] tile run starts (sorted order)
+    uint32_t* cur = loff + B4;                                // [B4] this CTA's next global position per bucket
+    uint32_t* rbase = cur + B4;                               // [B4] global position of run b minus its sorted start
+    uint32_t* tmp = rbase + B4;                               // [64]
+    uint32_t* DIR = tmp + 64;                                 // [kBkBins]
+    bk_stage_dir(p, MS, DIR);
+    // bucket starts (exclusive scan of the bucket sizes) + this CTA's prefix within each bucket
+    for (uint32_t b = threadIdx.x; b < B; b += blockDim.x) { cur[b] = p.tot[b]; hist[b] = 0; }
+    __syncthreads();
+    bk_exscan(cur, B, tmp);
+    for (uint32_t b = threadIdx.x; b < B; b += blockDim.x) cur[b] += p.cnt[(uint64_t)blockIdx.x * B + b];
+    const uint64_t pol = p.stream_hint ? policy_evict_first() : policy_evict_normal();
+    const uint64_t pol_run = policy_evict_normal();
+    const uint64_t ntiles = (p.m + T - 1) / T;
+    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const uint64_t b0 = t * T;
+        const uint32_t cntq = (uint32_t)((p.m - b0) < T ? (p.m - b0) : T);
+        K x[E];
+        uint32_t bb[E], rr[E];
+#pragma unroll
+        for (uint32_t e = 0; e < E; ++e) {
+            const uint32_t j = e * kBkPThreads + threadIdx.x;
+            x[e] = j < cntq ? load_stream(p.q + b0 + j, true, pol) : (K)0;
+        }
+        __syncthreads();   // hist is zero, cur is final, the previous tile's stores are done
+#pragma unroll
+        for (uint32_t e = 0; e < E; ++e) {
+            const uint32_t j = e * kBkPThreads + threadIdx.x;
+            bb[e] = 0xFFFFu;
+            if (j < cntq) {
+                bb[e] = bk_bucket(p, MS, DIR, x[e]);
+                rr[e] = atomicAdd(&hist[bb[e]], 1u);
+            }
+        }
+        __syncthreads();
+        for (uint32_t b = threadIdx.x; b < B; b += blockDim.x) loff[b] = hist[b];
+        __syncthreads();
+        bk_exscan(loff, B, tmp);
+        // the run of bucket b starts at cur[b] in the bucket-major array: P3 finds a
+        // sorted position s of bucket b there at (cur[b] - loff[b]) + s
+        for (uint32_t b = threadIdx.x; b < B; b += blockDim.x) {
+            const uint32_t rb = cur[b] - loff[b];
+            rbase[b] = rb;
+            p.trun[t * B + b] = rb;
+        }
+#pragma unroll
+        for (uint32_t e = 0; e < E; ++e) {
+            if (bb[e] == 0xFFFFu) continue;
+            const uint32_t sidx = loff[bb[e]] + rr[e];
+            stq[sidx] = x[e];
+            sbp[sidx] = bb[e] | ((e * kBkPThreads + threadIdx.x) << 16);
+        }
+        __syncthreads();
+        for (uint32_t b = threadIdx.x; b < B; b += blockDim.x) { cur[b] += hist[b]; hist[b] = 0; }
+        // each run to its place in its bucket's region (consecutive within a run;
+        // evict_normal: the run's partial lines are completed by this CTA's next
+        // tile and must stay in L2 until then), and the tile's (bucket, slot) list
+        for (uint32_t sidx = threadIdx.x; sidx < cntq; sidx += blockDim.x) {
+            const uint32_t w = sbp[sidx];
+            store_stream(p.rq + (uint32_t)(rbase[w & 0xFFFFu] + sidx), stq[sidx], true, pol_run);
+            store_stream(p.bp + b0 + sidx, w, true, pol);
+        }
+    }
+}
+
+// ---- pass 4: the per-bucket search
+//
+// One lookup: x's image under the bucket's parameters descends D levels of the
+// staged table (one 4-B shared load per level on the address recurrence
+// a' = 2a - sb + 4 [T[k] < q]), which gives c = #(leaf maxima images < q's) <= the
+// exact leaf; the 32-B leaf c then gives lb.  A leaf whose keys are all < q
+// (possible only when a leaf maximum's image ties q's) continues by galloping
+// over the real leaf maxima.
+// the rare image-tie continuation of a leaf scan: the first leaf l > c whose
+// maximum is >= x (galloping over the real leaf maxima), rescanned; returns
+// l | nlt << 32 | eq << 40
+template <class K>
+__device__ __noinline__ uint64_t bk_leaf_tie(const K* __restrict__ ab, uint64_t len, uint32_t Mb, uint32_t c, K x,
+                                             uint64_t pol_leaf) {
+    constexpr uint32_t LK = 32u / sizeof(K);
+    auto mxv = [&](uint32_t j) -> K {
+        const uint64_t e = ((uint64_t)j + 1) * LK;
+        return ldg(ab + (e < len ? e : len) - 1);
+    };
+    uint32_t l = c + 1, step = 1, h;
+    for (;;) {
+        h = l - 1 + step;
+        if (h >= Mb) { h = Mb; break; }
+        if (mxv(h) >= x) break;
+        l = h + 1;
+        step <<= 1;
+    }
+    while (l < h) {
+        const uint32_t mid = (l + h) >> 1;
+        if (mxv(mid) < x) l = mid + 1;
+        else h = mid;
+    }
+    uint32_t nlt = 0;
+    bool eq = false;
+    if (l < Mb) {
+        uint64_t w[4];
+        ld_sector(ab + (uint64_t)l * LK, pol_leaf, w);
+#pragma unroll
+        for (uint32_t u = 0; u < LK; ++u) {
+            const K v = bk_key<K>(w, (int)u);
+            nlt += v < x ? 1u : 0u;
+            eq |= v == x;
+        }
+    }
+    return (uint64_t)l | ((uint64_t)nlt << 32) | ((uint64_t)(eq ? 1u : 0u) << 40);
+}
+
+template <class K, int OB>
+__device__ __forceinline__ void bk_finish(const K* __restrict__ ab, uint64_t klo, uint64_t len, uint32_t Mb,
+                                          uint64_t n, K x, uint32_t c, const uint64_t* lv, void* rp, uint32_t ir,
+                                          uint64_t pol_leaf, uint64_t pol_stream) {
+    using O = typename std::conditional<OB == 8, uint64_t, uint32_t>::type;
+    constexpr uint32_t LK = 32u / sizeof(K);
+    uint64_t lb;
+    bool hit = false;
+    if (c >= Mb) {
+        lb = n;   // past every key of the (last) bucket
+    } else {
+        uint32_t nlt = 0;
+        bool eq = false;
+#pragma unroll
+        for (uint32_t u = 0; u < LK; ++u) {
+            const K v = bk_key<K>(lv, (int)u);
+            nlt += v < x ? 1u : 0u;
+            eq |= v == x;
+        }
+        if (__builtin_expect(nlt == LK && c + 1 < Mb, 0)) {
+            const uint64_t r = bk_leaf_tie<K>(ab, len, Mb, c, x, pol_leaf);
+            c = (uint32_t)r;
+            nlt = (uint32_t)(r >> 32) & 0xFFu;
+            eq = (r >> 40) & 1u;
+        }
+        lb = klo + (uint64_t)c * LK + nlt;
+        if (lb > n) lb = n;
+        hit = eq && lb < n;
+    }
+    constexpr uint64_t MISS = 1ull << (8 * OB - 1);
+    store_stream((O*)rp + ir, (O)(hit ? lb : (lb | MISS)), true, pol_stream);
+}
+
+// Items of CH queries in bucket order (CTA c takes items c, c + G, ...: the CTAs
+// work on a window of neighbouring buckets, whose slices of the array stay in
+// L2); the bucket's table is staged once per item that changes bucket.  R
+// lookups per thread descend together (their shared-memory latencies overlap).
+// Measured alternative: a software pipeline (leaves of batch k in flight while
+// batch k+1 descends) ran 3 % slower — the kernel is bound by the L1 data pipe
+// (shared-memory bank conflicts of the random probes + one leaf wavefront per
+// lookup), not by latency.
+template <class K, int OB, int D>
+__global__ void __launch_bounds__(kBkThreads, 1)
+k_bk_search(const BkParams<K> p) {
+    constexpr uint32_t LK = 32u / sizeof(K);
+    constexpr uint32_t R = 4;          // lookups in flight per thread
+    constexpr uint32_t S = 1u << D;
+    extern __shared__ __align__(16) uint32_t sm[];
+    const uint32_t B = p.B;
+    uint32_t* Tab = sm;                                     // [2^D]
+    uint32_t* bst = Tab + S;                                // [B + 1] bucket starts
+    uint32_t* ipre = bst + ((B + 4u) & ~3u);                // [B + 1] first item of each bucket
+    uint32_t* tmp = ipre + ((B + 4u) & ~3u);                // [64]
+    uint64_t* bar = reinterpret_cast<uint64_t*>(tmp + 64);
+    for (uint32_t b = threadIdx.x; b < B; b += blockDim.x) {
+        const uint32_t t = p.tot[b];
+        bst[b] = t;
+        ipre[b] = (t + p.CH - 1) / p.CH;
+    }
+    __syncthreads();
+    const uint32_t mtot = bk_exscan(bst, B, tmp);
+    const uint32_t I = bk_exscan(ipre, B, tmp);
+    if (threadIdx.x == 0) { bst[B] = mtot; ipre[B] = I; }
+    __syncthreads();
+    const uint64_t pol_stream = p.stream_hint ? policy_evict_first() : policy_evict_normal();
+    const uint64_t pol_leaf = policy_evict_normal();
+    const uint32_t sb = smem_u32(Tab);
+    const uint32_t step_lt = 4u - sb, step_ge = 0u - sb;
+    uint32_t staged = 0xFFFFFFFFu;
+    for (uint32_t it = blockIdx.x; it < I; it += gridDim.x) {
+        // bucket of item it: the last b with ipre[b] <= it (it has items, so ipre[b+1] > it)
+        uint32_t lo = 0, hi = B;
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (ipre[mid] <= it) lo = mid;
+            else hi = mid;
+        }
+        const uint32_t b = lo;
+        const uint32_t i0 = bst[b] + (it - ipre[b]) * p.CH;
+        const uint32_t i1 = min(i0 + p.CH, bst[b + 1]);
+        if (b != staged) {
+            __syncthreads();   // every lookup of the previous item is done with Tab
+            stage_to_smem(Tab, p.tab + ((uint64_t)b << D), 4u << D, bar);
+            staged = b;
+        }
+        const uint64_t base = p.par[2 * b];
+        const uint32_t sh = (uint32_t)p.par[2 * b + 1];
+        const uint64_t klo = (uint64_t)b * p.NB;
+        const uint64_t len = (p.n - klo) < p.NB ? (p.n - klo) : p.NB;
+        const uint32_t Mb = (uint32_t)((len + LK - 1) / LK);
+        const K* ab = p.a + klo;
+        for (uint32_t i = i0 + threadIdx.x; i < i1; i += kBkThreads * R) {
+            K x[R];
+            uint32_t ad[R], fq[R];
+#pragma unroll
+            for (uint32_t r = 0; r < R; ++r) {
+                const uint32_t ir = i + r * kBkThreads;
+                x[r] = ir < i1 ? load_stream(p.rq + ir, true, pol_stream) : (K)base;
+                fq[r] = bk_img((uint64_t)x[r], base, sh);
+                ad[r] = sb + 4u;
+            }
+#pragma unroll
+            for (uint32_t d = 0; d < (uint32_t)D; ++d) {
+#pragma unroll
+                for (uint32_t r = 0; r < R; ++r) {
+                    const uint32_t h = lds_u32(ad[r]);
+                    ad[r] = 2u * ad[r] + (h < fq[r] ? step_lt : step_ge);
+                }
+            }
+            uint64_t lv[R][4];
+            uint32_t c[R];
+#pragma unroll
+            for (uint32_t r = 0; r < R; ++r) {
+                c[r] = ((ad[r] - sb) >> 2) - S;
+                if (c[r] < Mb) ld_sector(ab + (uint64_t)c[r] * LK, pol_leaf, lv[r]);
+            }
+#pragma unroll
+            for (uint32_t r = 0; r < R; ++r) {
+                const uint32_t ir = i + r * kBkThreads;
+                if (ir < i1) bk_finish<K, OB>(ab, klo, len, Mb, p.n, x[r], c[r], lv[r], p.rp, ir, pol_leaf, pol_stream);
+            }
+        }
+    }
+}
+
+// ---- pass 5: back to query order (any grid: the run bases are stored per tile)
+template <class K, int OB>
+__global__ void __launch_bounds__(kBkPThreads, 4)
+k_bk_unpart(const BkParams<K> p) {
+    using O = typename std::conditional<OB == 8, uint64_t, uint32_t>::type;
+    constexpr uint32_t T = kBkTile, E = T / kBkPThreads;
+    extern __shared__ __align__(16) uint32_t sm[];
+    O* so = reinterpret_cast<O*>(sm);                         // [T] results, query order
+    uint32_t* rb = reinterpret_cast<uint32_t*>(so + T);       // [B]
+    const uint32_t B = p.B;
+    const uint64_t pol = p.stream_hint ? policy_evict_first() : policy_evict_normal();
+    const uint64_t ntiles = (p.m + T - 1) / T;
+    const uint64_t pol_run = policy_evict_normal();   // runs share lines with the neighbouring tiles' runs
+    const O* rp = (const O*)p.rp;
+    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const uint64_t b0 = t * T;
+        const uint32_t cntq = (uint32_t)((p.m - b0) < T ? (p.m - b0) : T);
+        for (uint32_t b = threadIdx.x; b < B; b += blockDim.x) rb[b] = p.trun[t * B + b];
+        uint32_t bp[E];   // bucket | slot << 16
+#pragma unroll
+        for (uint32_t e = 0; e < E; ++e) {
+            const uint32_t s = e * kBkPThreads + threadIdx.x;
+            bp[e] = s < cntq ? load_stream(p.bp + b0 + s, true, pol) : 0u;
+        }
+        __syncthreads();   // rb is in place; the previous tile's stores have read `so`
+        // gathers in two halves of E/2 loads in flight (32 registers: two CTAs per SM)
+#pragma unroll
+        for (uint32_t h = 0; h < E; h += E / 2) {
+            O v[E / 2];
+#pragma unroll
+            for (uint32_t e = 0; e < E / 2; ++e) {
+                const uint32_t s = (h + e) * kBkPThreads + threadIdx.x;
+                if (s < cntq) v[e] = load_stream(rp + (uint32_t)(rb[bp[h + e] & 0xFFFFu] + s), true, pol_run);
+            }
+#pragma unroll
+            for (uint32_t e = 0; e < E / 2; ++e) {
+                const uint32_t s = (h + e) * kBkPThreads + threadIdx.x;
+                if (s < cntq) so[bp[h + e] >> 16] = v[e];
+            }
+        }
+        __syncthreads();
+        O* out = (O*)p.out + b0;
+        if (cntq == T && OB == 8) {
+            // 16-B stores: two results per thread per step
+            for (uint32_t j = threadIdx.x * 2; j < T; j += blockDim.x * 2) {
+                const uint2 lo = *reinterpret_cast<const uint2*>(so + j);
+                const uint2 hi = *reinterpret_cast<const uint2*>(so + j + 1);
+                asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;"
+                             :: "l"(out + j), "r"(lo.x), "r"(lo.y), "r"(hi.x), "r"(hi.y), "l"(pol) : "memory");
+            }
+        } else {
+            for (uint32_t j = threadIdx.x; j < cntq; j += blockDim.x) store_stream(out + j, so[j], true, pol);
+        }
+    }
+}
+
+// ------------------------------------------------------------------ host
+
+struct BkLayout {
+    uint64_t G, Gs, B, ntiles;
+    uint64_t o_cnt, o_tot, o_rq, o_rp, o_bp, o_trun, total;
+};
+
+static bool bk_layout(uint64_t B, uint64_t m, int kb, int ob, uint32_t sm_count, BkLayout* L) {
+    if (B == 0 || B > kBkMaxBuckets || m >= (1ull << 32)) return false;
+    L->G = 2ull * sm_count;   // two CTAs of kBkPThreads per SM (hist / part; unpart runs four)
+    L->Gs = sm_count;
+    L->B = B;
+    L->ntiles = (m + kBkTile - 1) / kBkTile;
+    const uint64_t mm = m ? m : 1;
+    uint64_t o = 0;
+    auto take = [&](uint64_t bytes) { const uint64_t r = o; o += (bytes + 255) & ~255ull; return r; };
+    L->o_cnt = take(4 * L->G * B);
+    L->o_tot = take(4 * B);
+    L->o_rq = take((uint64_t)kb * mm);
+    L->o_rp = take((uint64_t)ob * mm);
+    L->o_bp = take(4 * mm);
+    L->o_trun = take(4 * L->ntiles * B);
+    L->total = o;
+    return true;
+}
+
+bool bucket_workspace_bytes(uint64_t B, uint64_t m, int kb, int ob, uint32_t sm_count, uint64_t* bytes) {
+    BkLayout L;
+    if (!bk_layout(B, m, kb, ob, sm_count, &L)) return false;
+    *bytes = L.total;
+    return true;
+}
+
+static cudaError_t bk_launch(const void* kern, uint32_t threads, uint32_t smem, uint32_t blocks, const void* params,
+                             cudaStream_t s) {
+    bool uns = false;
+    uint64_t g = 0;
+    Grid grid{0u, 1u, blocks};
+    cudaError_t e = plan_grid(kern, threads, smem, grid, blocks, carveout_for(smem, threads), &g, &uns);
+    if (e != cudaSuccess) return e;
+    if (uns) return cudaErrorInvalidConfiguration;
+    void* args[] = {const_cast<void*>(params)};
+    e = cudaLaunchKernel(kern, dim3(blocks), dim3(threads), args, smem, s);
+    count_launch();
+    return e;
+}
+
+template <class K, int OB>
+static cudaError_t go_bucket(BkParams<K> p, const BkLayout& L, char* ws, cudaStream_t s) {
+    p.G = (uint32_t)L.G;
+    p.Gs = (uint32_t)L.Gs;
+    p.cnt = (uint32_t*)(ws + L.o_cnt);
+    p.tot = (uint32_t*)(ws + L.o_tot);
+    p.rq = (K*)(ws + L.o_rq);
+    p.rp = ws + L.o_rp;
+    p.bp = (uint32_t*)(ws + L.o_bp);
+    p.trun = (uint32_t*)(ws + L.o_trun);
+    const uint32_t B = p.B, B4 = (B + 3u) & ~3u;
+    cudaError_t e;
+    {
+        const uint32_t smem = 8u * B4 + 4u * kBkBins;
+        e = bk_launch((const void*)k_bk_hist<K>, kBkPThreads, smem, p.G, &p, s);
+        if (e != cudaSuccess) return e;
+    }
+    k_bk_scan<<<(B + 31) / 32, 1024, 0, s>>>(p.cnt, p.tot, p.G, B);
+    count_launch();
+    {
+        const uint32_t smem = kBkTile * ((uint32_t)sizeof(K) + 4u) + 4u * (5u * B4 + 64u) + 4u * kBkBins;
+        e = bk_launch((const void*)k_bk_part<K>, kBkPThreads, smem, p.G, &p, s);
+        if (e != cudaSuccess) return e;
+    }
+    {
+        const uint32_t smem = (4u << p.D) + 8u * ((B + 4u) & ~3u) + 4u * 64u + 16u;
+        const void* kern = p.D == 15 ? (const void*)k_bk_search<K, OB, 15>
+                         : p.D == 14 ? (const void*)k_bk_search<K, OB, 14> : nullptr;
+        if (!kern) return cudaErrorInvalidValue;
+        e = bk_launch(kern, kBkThreads, smem, p.Gs, &p, s);
+        if (e != cudaSuccess) return e;
+    }
+    {
+        const uint32_t smem = kBkTile * OB + 4u * B4;
+        e = bk_launch((const void*)k_bk_unpart<K, OB>, kBkPThreads, smem, 2u * p.G, &p, s);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bucket(int kb, int ob, const BucketIndex& bi, const void* a, uint64_t n, const void* q, uint64_t m,
+                          void* out, uint32_t stream_hint, uint32_t chunk, void* ws, uint64_t ws_bytes,
+                          uint32_t sm_count, cudaStream_t s, bool* uns) {
+    BkLayout L;
+    if (!bi.tab || !bk_layout(bi.B, m, kb, ob, sm_count, &L) || ws_bytes < L.total) { *uns = true; return cudaSuccess; }
+    auto fill = [&](auto& p) {
+        p.n = n; p.m = m; p.out = out; p.stream_hint = stream_hint;
+        p.B = (uint32_t)bi.B; p.D = bi.D; p.NB = (1ull << bi.D) * (32u / (uint32_t)kb);
+        p.tab = bi.tab; p.par = bi.par; p.mx = bi.mx; p.dir = bi.dir;
+        p.gbase = bi.gbase; p.gsh = bi.gsh;
+        p.CH = chunk ? chunk : kBkChunk;
+    };
+    if (kb == 8) {
+        BkParams<uint64_t> p{};
+        fill(p);
+        p.a = (const uint64_t*)a; p.q = (const uint64_t*)q;
+        return ob == 8 ? go_bucket<uint64_t, 8>(p, L, (char*)ws, s) : go_bucket<uint64_t, 4>(p, L, (char*)ws, s);
+    }
+    BkParams<uint32_t> p{};
+    fill(p);
+    p.a = (const uint32_t*)a; p.q = (const uint32_t*)q;
+    return ob == 8 ? go_bucket<uint32_t, 8>(p, L, (char*)ws, s) : go_bucket<uint32_t, 4>(p, L, (char*)ws, s);
+}
+
+}  // namespace bs

@@ -1,5 +1,5 @@
 """Aggregate an ncu source page (cuda,sass) by CUDA source line: instructions
-executed and stall samples.  python tools/ncu_lines.py rep.ncu-rep [top]"""
+executed and stall samples.  python tools/ncu_lines.py rep.ncu-rep [top] [kernel-regex]"""
 import csv
 import io
 import subprocess
@@ -7,7 +7,8 @@ import sys
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
-txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+kfilter = ["--kernel-name", "regex:" + sys.argv[3]] if len(sys.argv) > 3 else []
+txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass", *kfilter],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(txt)))
 agg = {}
