@@ -113,7 +113,7 @@ cudaError_t plan_grid(const void* kern, uint32_t threads, uint32_t smem, Grid gr
     return cudaSuccess;
 }
 
-static uint64_t bucket_max_keys(uint32_t kb) { return (uint64_t)kBkMaxBuckets << 15 << (kb == 8 ? 2 : 3); }
+static uint64_t bucket_max_keys(uint32_t kb) { return (uint64_t)kBkMaxBuckets * (kBkCoarseBytes / kb); }
 
 static bool is_pow2(uint64_t x) { return x && !(x & (x - 1)); }
 
@@ -384,25 +384,36 @@ const char* bs_version(void) {
     return "libbs 0.1 (sm_100a; naive / opt / kary; arXiv 2506.01576)";
 }
 
-// Buckets of 2^D leaves of 32 B (D = 15; BS_BUCKET_D = 14 for A/B runs): the
-// tables, per-bucket image parameters, bucket maxima and their directory in one
-// allocation.  Not built (the mode reports UNSUPPORTED) above kBkMaxBuckets.
+// BS_REORDER_BUCKET structures (part.cu).  Fine: buckets of 2^D leaves of 32 B
+// (D = 15; BS_BUCKET_D = 14 for A/B runs) with their pinned tables, while that
+// needs <= kBkFineMax buckets (n <= 2^27 u64 / 2^28 u32 keys); coarse above:
+// buckets of kBkCoarseBytes of keys (searched by the index's own kernel), up to
+// kBkMaxBuckets.  Tables, per-bucket image parameters, bucket maxima and their
+// directory in one allocation.  Not built (the mode reports UNSUPPORTED) above that.
 static int build_bucket_layout(Index* ix, cudaStream_t st, BuildTimer& bt) {
     uint32_t D = 15;
     if (const char* v = getenv("BS_BUCKET_D")) D = (uint32_t)atoi(v) == 14 ? 14u : 15u;
-    const uint64_t NB = (1ull << D) * (32u / ix->kb);
-    const uint64_t B = (ix->n + NB - 1) / NB;
+    const bool force_coarse = getenv("BS_BUCKET_COARSE") && atoi(getenv("BS_BUCKET_COARSE")) != 0;
+    uint64_t NB = (1ull << D) * (32u / ix->kb);
+    uint64_t B = (ix->n + NB - 1) / NB;
+    if (B > kBkFineMax || force_coarse) {
+        D = 0;
+        NB = kBkCoarseBytes / ix->kb;
+        B = (ix->n + NB - 1) / NB;
+    }
     if (B > kBkMaxBuckets) return BS_OK;
     cudaError_t e = cudaStreamSynchronize(st);   // a_first / a_last are on the host
     if (e != cudaSuccess) return fail_cuda(e, "bucket tables: sync");
     auto al = [](uint64_t x) { return (x + 255) & ~255ull; };
-    const uint64_t o_tab = 0, o_par = al(4 * (B << D)), o_mx = o_par + al(16 * B), o_dir = o_mx + al(4 * B);
+    const uint64_t tab_bytes = D ? al(4 * (B << D)) : 0, par_bytes = D ? al(16 * B) : 0;
+    const uint64_t o_tab = 0, o_par = tab_bytes, o_mx = o_par + par_bytes, o_dir = o_mx + al(4 * B);
     const uint64_t total = o_dir + al(2 * ((1u << 13) + 1));
     e = cudaMalloc(&ix->d_bk, total);
     if (e != cudaSuccess) return fail_cuda(e, "cudaMalloc(bucket tables)");
     BucketIndex& bi = ix->bk;
     char* p = (char*)ix->d_bk;
     bi.B = B;
+    bi.NB = NB;
     bi.D = D;
     bi.gbase = ix->a_first;
     const uint64_t span = ix->a_last - ix->a_first;
@@ -410,12 +421,12 @@ static int build_bucket_layout(Index* ix, cudaStream_t st, BuildTimer& bt) {
     while (bl < 64 && (span >> bl) != 0) ++bl;
     bi.gsh = bl > 32 ? bl - 32 : 0;
     bt.begin(kStImg);
-    e = build_bucket_index(ix->kb, ix->d_keys, ix->n, D, B, bi.gbase, bi.gsh, (uint32_t*)(p + o_tab),
-                           (uint64_t*)(p + o_par), (uint32_t*)(p + o_mx), (uint16_t*)(p + o_dir), st);
+    e = build_bucket_index(ix->kb, ix->d_keys, ix->n, D, NB, B, bi.gbase, bi.gsh, D ? (uint32_t*)(p + o_tab) : nullptr,
+                           D ? (uint64_t*)(p + o_par) : nullptr, (uint32_t*)(p + o_mx), (uint16_t*)(p + o_dir), st);
     bt.end();
     if (e != cudaSuccess) return fail_cuda(e, "build_bucket_index");
-    bi.tab = (const uint32_t*)(p + o_tab);
-    bi.par = (const uint64_t*)(p + o_par);
+    bi.tab = D ? (const uint32_t*)(p + o_tab) : nullptr;
+    bi.par = D ? (const uint64_t*)(p + o_par) : nullptr;
     bi.mx = (const uint32_t*)(p + o_mx);
     bi.dir = (const uint16_t*)(p + o_dir);
     ix->bk_bytes = total;
@@ -698,7 +709,7 @@ static int lookup_impl(const void* idx, const void* queries, uint64_t m, void* o
     }
     if (L.reorder == BS_REORDER_BUCKET) {
         uint64_t need = 0;
-        if (!ix->bk.tab || !bucket_workspace_bytes(ix->bk.B, m, ix->kb, ix->ob, (uint32_t)ix->sm_count, &need))
+        if (!ix->bk.mx || !bucket_workspace_bytes(ix->bk.B, m, ix->kb, ix->ob, (uint32_t)ix->sm_count, &need))
             return fail(BS_ERR_UNSUPPORTED, "BS_REORDER_BUCKET: needs n <= %llu keys and m < 2^32",
                         (unsigned long long)bucket_max_keys(ix->kb));
         if (!ws) return fail(BS_ERR_INVALID, "BS_REORDER_BUCKET needs a workspace: bs_lookup_ws");
@@ -709,11 +720,39 @@ static int lookup_impl(const void* idx, const void* queries, uint64_t m, void* o
         bool uns = false;
         uint32_t chunk = 0;
         if (const char* v = getenv("BS_BUCKET_CHUNK")) chunk = (uint32_t)atoi(v);
-        cudaError_t e = launch_bucket(ix->kb, ix->ob, ix->bk, ix->d_keys, ix->n, queries, m, out,
-                                      (L.cache_hints & BS_HINT_STREAM_EVICT_FIRST) ? 1u : 0u, chunk, ws, ws_bytes,
-                                      (uint32_t)ix->sm_count, (cudaStream_t)stream, &uns);
+        const uint32_t hint = (L.cache_hints & BS_HINT_STREAM_EVICT_FIRST) ? 1u : 0u;
+        cudaStream_t s = (cudaStream_t)stream;
+        if (ix->bk.tab) {   // fine buckets: the whole pipeline in part.cu
+            cudaError_t e = launch_bucket(ix->kb, ix->ob, ix->bk, ix->d_keys, ix->n, queries, m, out, hint, chunk, ws,
+                                          ws_bytes, (uint32_t)ix->sm_count, s, &uns, 0, nullptr);
+            if (uns) return fail(BS_ERR_UNSUPPORTED, "BS_REORDER_BUCKET: not supported for this index / batch");
+            if (e != cudaSuccess) return fail_cuda(e, "bucket partition launch");
+            return BS_OK;
+        }
+        // coarse buckets: partition, the index's own kernel over the partitioned
+        // batch (its array accesses now move through one L2-sized slice at a time),
+        // then back to query order
+        BucketRun run;
+        cudaError_t e = launch_bucket(ix->kb, ix->ob, ix->bk, ix->d_keys, ix->n, queries, m, out, hint, chunk, ws,
+                                      ws_bytes, (uint32_t)ix->sm_count, s, &uns, 1, &run);
         if (uns) return fail(BS_ERR_UNSUPPORTED, "BS_REORDER_BUCKET: not supported for this index / batch");
         if (e != cudaSuccess) return fail_cuda(e, "bucket partition launch");
+        bs_launch Lk = L;
+        Lk.reorder = BS_REORDER_NONE;
+        // the partitioned batch reuses each leaf line while its slice is worked
+        // on: leaves must not be marked evict_first (the default for arrays > 2 L2)
+        Lk.cache_hints &= ~BS_HINT_LEAF_EVICT_FIRST;
+        // one persistent launch over the whole partitioned batch.  Measured
+        // alternatives (config 4): a warp-ticket schedule that keeps every warp
+        // within one chunk of the batch front cut the kernel's DRAM reads from 109
+        // to 17 B / lookup but ran slower (44 vs 39 ms: on L2-hot slices this
+        // kernel is bound by issue and dependent L2 round trips, not DRAM), as did
+        // two lookups per thread (64 ms) and one launch per 2^22 queries
+        const int rc = dispatch_lookup(ix, run.rq, m, run.rp, s, Lk);
+        if (rc != BS_OK) return rc;
+        e = launch_bucket(ix->kb, ix->ob, ix->bk, ix->d_keys, ix->n, queries, m, out, hint, chunk, ws, ws_bytes,
+                          (uint32_t)ix->sm_count, s, &uns, 2, nullptr);
+        if (e != cudaSuccess) return fail_cuda(e, "bucket unpartition launch");
         return BS_OK;
     }
     return dispatch_lookup(ix, queries, m, out, (cudaStream_t)stream, L);
@@ -740,7 +779,7 @@ int bs_workspace_bytes(const void* idx, uint64_t m, const bs_launch* launch, uin
     }
     *bytes = 0;
     if (L.reorder == BS_REORDER_BUCKET) {
-        if (!ix->bk.tab || !bucket_workspace_bytes(ix->bk.B, m, ix->kb, ix->ob, (uint32_t)ix->sm_count, bytes))
+        if (!ix->bk.mx || !bucket_workspace_bytes(ix->bk.B, m, ix->kb, ix->ob, (uint32_t)ix->sm_count, bytes))
             return fail(BS_ERR_UNSUPPORTED, "BS_REORDER_BUCKET: needs n <= %llu keys and m < 2^32",
                         (unsigned long long)bucket_max_keys(ix->kb));
         return BS_OK;

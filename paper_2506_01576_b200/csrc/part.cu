@@ -126,21 +126,19 @@ __global__ void k_bk_build_dir(const K* __restrict__ a, uint64_t n, uint64_t NB,
     }
 }
 
-cudaError_t build_bucket_index(int kb, const void* a, uint64_t n, uint32_t D, uint64_t B, uint64_t gbase,
+cudaError_t build_bucket_index(int kb, const void* a, uint64_t n, uint32_t D, uint64_t NB, uint64_t B, uint64_t gbase,
                                uint32_t gsh, uint32_t* tab, uint64_t* par, uint32_t* mx, uint16_t* dir,
                                cudaStream_t s) {
     const uint32_t LK = 32u / (uint32_t)kb;
-    const uint64_t NB = (1ull << D) * LK;
-    const uint64_t tot = B << D;
-    const uint32_t g1 = (uint32_t)((tot + 255) / 256);
     const uint32_t g2 = (uint32_t)(((B > kBkBins + 1 ? B : kBkBins + 1) + 255) / 256);
-    if (kb == 8) {
-        k_bk_build_tab<uint64_t><<<g1, 256, 0, s>>>((const uint64_t*)a, n, D, LK, B, tab, par);
-        k_bk_build_dir<uint64_t><<<g2, 256, 0, s>>>((const uint64_t*)a, n, NB, (uint32_t)B, gbase, gsh, mx, dir);
-    } else {
-        k_bk_build_tab<uint32_t><<<g1, 256, 0, s>>>((const uint32_t*)a, n, D, LK, B, tab, par);
-        k_bk_build_dir<uint32_t><<<g2, 256, 0, s>>>((const uint32_t*)a, n, NB, (uint32_t)B, gbase, gsh, mx, dir);
+    if (tab) {
+        const uint64_t tot = B << D;
+        const uint32_t g1 = (uint32_t)((tot + 255) / 256);
+        if (kb == 8) k_bk_build_tab<uint64_t><<<g1, 256, 0, s>>>((const uint64_t*)a, n, D, LK, B, tab, par);
+        else k_bk_build_tab<uint32_t><<<g1, 256, 0, s>>>((const uint32_t*)a, n, D, LK, B, tab, par);
     }
+    if (kb == 8) k_bk_build_dir<uint64_t><<<g2, 256, 0, s>>>((const uint64_t*)a, n, NB, (uint32_t)B, gbase, gsh, mx, dir);
+    else k_bk_build_dir<uint32_t><<<g2, 256, 0, s>>>((const uint32_t*)a, n, NB, (uint32_t)B, gbase, gsh, mx, dir);
     return cudaGetLastError();
 }
 
@@ -698,7 +696,7 @@ static cudaError_t bk_launch(const void* kern, uint32_t threads, uint32_t smem, 
 }
 
 template <class K, int OB>
-static cudaError_t go_bucket(BkParams<K> p, const BkLayout& L, char* ws, cudaStream_t s) {
+static cudaError_t go_bucket(BkParams<K> p, const BkLayout& L, char* ws, cudaStream_t s, int phase, BucketRun* run) {
     p.G = (uint32_t)L.G;
     p.Gs = (uint32_t)L.Gs;
     p.cnt = (uint32_t*)(ws + L.o_cnt);
@@ -707,21 +705,24 @@ static cudaError_t go_bucket(BkParams<K> p, const BkLayout& L, char* ws, cudaStr
     p.rp = ws + L.o_rp;
     p.bp = (uint32_t*)(ws + L.o_bp);
     p.trun = (uint32_t*)(ws + L.o_trun);
+    if (run) { run->rq = p.rq; run->rp = p.rp; }
     const uint32_t B = p.B, B4 = (B + 3u) & ~3u;
     cudaError_t e;
-    {
-        const uint32_t smem = 8u * B4 + 4u * kBkBins;
-        e = bk_launch((const void*)k_bk_hist<K>, kBkPThreads, smem, p.G, &p, s);
-        if (e != cudaSuccess) return e;
+    if (phase != 2) {
+        {
+            const uint32_t smem = 8u * B4 + 4u * kBkBins;
+            e = bk_launch((const void*)k_bk_hist<K>, kBkPThreads, smem, p.G, &p, s);
+            if (e != cudaSuccess) return e;
+        }
+        k_bk_scan<<<(B + 31) / 32, 1024, 0, s>>>(p.cnt, p.tot, p.G, B);
+        count_launch();
+        {
+            const uint32_t smem = kBkTile * ((uint32_t)sizeof(K) + 4u) + 4u * (5u * B4 + 64u) + 4u * kBkBins;
+            e = bk_launch((const void*)k_bk_part<K>, kBkPThreads, smem, p.G, &p, s);
+            if (e != cudaSuccess) return e;
+        }
     }
-    k_bk_scan<<<(B + 31) / 32, 1024, 0, s>>>(p.cnt, p.tot, p.G, B);
-    count_launch();
-    {
-        const uint32_t smem = kBkTile * ((uint32_t)sizeof(K) + 4u) + 4u * (5u * B4 + 64u) + 4u * kBkBins;
-        e = bk_launch((const void*)k_bk_part<K>, kBkPThreads, smem, p.G, &p, s);
-        if (e != cudaSuccess) return e;
-    }
-    {
+    if (phase == 0) {
         const uint32_t smem = (4u << p.D) + 8u * ((B + 4u) & ~3u) + 4u * 64u + 16u;
         const void* kern = p.D == 15 ? (const void*)k_bk_search<K, OB, 15>
                          : p.D == 14 ? (const void*)k_bk_search<K, OB, 14> : nullptr;
@@ -729,7 +730,7 @@ static cudaError_t go_bucket(BkParams<K> p, const BkLayout& L, char* ws, cudaStr
         e = bk_launch(kern, kBkThreads, smem, p.Gs, &p, s);
         if (e != cudaSuccess) return e;
     }
-    {
+    if (phase != 1) {
         const uint32_t smem = kBkTile * OB + 4u * B4;
         e = bk_launch((const void*)k_bk_unpart<K, OB>, kBkPThreads, smem, 2u * p.G, &p, s);
         if (e != cudaSuccess) return e;
@@ -739,12 +740,15 @@ static cudaError_t go_bucket(BkParams<K> p, const BkLayout& L, char* ws, cudaStr
 
 cudaError_t launch_bucket(int kb, int ob, const BucketIndex& bi, const void* a, uint64_t n, const void* q, uint64_t m,
                           void* out, uint32_t stream_hint, uint32_t chunk, void* ws, uint64_t ws_bytes,
-                          uint32_t sm_count, cudaStream_t s, bool* uns) {
+                          uint32_t sm_count, cudaStream_t s, bool* uns, int phase, BucketRun* run) {
     BkLayout L;
-    if (!bi.tab || !bk_layout(bi.B, m, kb, ob, sm_count, &L) || ws_bytes < L.total) { *uns = true; return cudaSuccess; }
+    if (!bi.mx || (phase == 0 && !bi.tab) || !bk_layout(bi.B, m, kb, ob, sm_count, &L) || ws_bytes < L.total) {
+        *uns = true;
+        return cudaSuccess;
+    }
     auto fill = [&](auto& p) {
         p.n = n; p.m = m; p.out = out; p.stream_hint = stream_hint;
-        p.B = (uint32_t)bi.B; p.D = bi.D; p.NB = (1ull << bi.D) * (32u / (uint32_t)kb);
+        p.B = (uint32_t)bi.B; p.D = bi.D; p.NB = bi.NB;
         p.tab = bi.tab; p.par = bi.par; p.mx = bi.mx; p.dir = bi.dir;
         p.gbase = bi.gbase; p.gsh = bi.gsh;
         p.CH = chunk ? chunk : kBkChunk;
@@ -753,12 +757,14 @@ cudaError_t launch_bucket(int kb, int ob, const BucketIndex& bi, const void* a, 
         BkParams<uint64_t> p{};
         fill(p);
         p.a = (const uint64_t*)a; p.q = (const uint64_t*)q;
-        return ob == 8 ? go_bucket<uint64_t, 8>(p, L, (char*)ws, s) : go_bucket<uint64_t, 4>(p, L, (char*)ws, s);
+        return ob == 8 ? go_bucket<uint64_t, 8>(p, L, (char*)ws, s, phase, run)
+                       : go_bucket<uint64_t, 4>(p, L, (char*)ws, s, phase, run);
     }
     BkParams<uint32_t> p{};
     fill(p);
     p.a = (const uint32_t*)a; p.q = (const uint32_t*)q;
-    return ob == 8 ? go_bucket<uint32_t, 8>(p, L, (char*)ws, s) : go_bucket<uint32_t, 4>(p, L, (char*)ws, s);
+    return ob == 8 ? go_bucket<uint32_t, 8>(p, L, (char*)ws, s, phase, run)
+                   : go_bucket<uint32_t, 4>(p, L, (char*)ws, s, phase, run);
 }
 
 }  // namespace bs

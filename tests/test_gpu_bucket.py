@@ -140,3 +140,23 @@ def test_bucket_config3_sample():
     assert np.array_equal(P.to_numpy_unsigned(out, 8)[samp], oracle.lookup(kh, qh[samp], out_bytes=8))
     assert bench.invariant_all(dk, dq, out, 8)
     idx.close()
+
+
+# ------------------------------------------------------------------ coarse buckets (large arrays)
+
+@pytest.mark.parametrize("kb", [4, 8])
+@pytest.mark.parametrize("variant", [bs.KARY, bs.OPT, bs.NAIVE])
+def test_bucket_coarse(kb, variant, monkeypatch):
+    """Coarse buckets (slices of 16 MB of keys, searched by the index's own kernel
+    over the partitioned batch) — the layout bs_build picks for arrays above 2^27
+    u64 / 2^28 u32 keys; forced here with BS_BUCKET_COARSE=1 on arrays of a few slices."""
+    monkeypatch.setenv("BS_BUCKET_COARSE", "1")
+    per = (16 << 20) // kb
+    n = 2 * per + 12345
+    keys = workload.gen_keys(n, kb, seed=900 + kb + variant)
+    for order in ("random", "sorted"):
+        q = queries_for(keys, 150000, 901, order)
+        for ob in ((4, 8) if kb == 4 else (8,)):
+            idx = build(keys, variant=variant, out_bytes=ob)
+            check(bk_run(idx, q, ob), oracle.lookup(keys, q, out_bytes=ob), q, f"coarse kb={kb} v={variant} {order} ob={ob}")
+            idx.close()
