@@ -61,6 +61,8 @@ CONFIGS = {
 }
 METRIC = "lookups/sec at 1/2/4/8 B200 (2^26 u64 keys, 2^27 random queries); % HBM roofline"
 VARIANTS = {"naive": 0, "opt": 1, "kary": 2}
+REORDER_NAMES = {0: "none", 1: "lookup", 2: "full", 3: "sorted (segment-staged)", 4: "global (2048 segments)",
+                 5: "bucket (key-range partition, L2-sized buckets)"}
 MISS64 = np.uint64(1 << 63)
 
 
@@ -82,6 +84,19 @@ def algorithmic_bytes_per_lookup(cfg: str, kb: int, ob: int, order: str, n: int,
     if CONFIGS[cfg][4] == "partitioned":
         return base + 2 * (kb + 4) + 2 * 8, "key + out + 32 + exchange (2 x (key + tag) + 2 x result)"
     return base, "key + out + 32 (one DRAM sector per lookup)"
+
+
+def default_reorder(cfg: str, order: str) -> int:
+    """The mode bench.py times by default: the key-range
+    partition (BS_REORDER_BUCKET) for a random batch over an array much larger
+    than L2, the segment-staged lookup (BS_REORDER_SORTED) for a sorted batch,
+    the plain K-ary kernel otherwise (L2-resident arrays, the peer path)."""
+    n, kb, _, _, mode, _ = CONFIGS[cfg]
+    if mode == "partitioned":
+        return 0
+    if order == "sorted":
+        return 3
+    return 5 if n * kb > (256 << 20) else 0
 
 
 def peaks():
@@ -427,7 +442,9 @@ def main():
     ap.add_argument("--leaf-chunk", type=int, default=0)
     ap.add_argument("--threads", type=int, default=0)
     ap.add_argument("--nreg", type=int, default=0)
-    ap.add_argument("--reorder", type=int, default=0)
+    ap.add_argument("--reorder", type=int, default=-1,
+                    help="bs_reorder; -1 = the config's fastest mode: BUCKET (5) for a random batch over an "
+                         "array larger than L2 (configs 3-4), SORTED (3) for a pre-sorted batch, else NONE")
     ap.add_argument("--schedule", type=int, default=1)
     ap.add_argument("--hints", type=int, default=0x100, help="cache_hints bits; 256 = BS_HINT_AUTO (resolved at build)")
     ap.add_argument("--kary-mode", type=int, default=8,
@@ -469,6 +486,8 @@ def main():
     cfg = args.config
     n, kb, m_cfg, hr, mode, desc = CONFIGS[cfg]
     ob = 8 if mode == "partitioned" else kb
+    if args.reorder < 0:
+        args.reorder = default_reorder(cfg, args.order)
     say("generating inputs")
     dk, dq, (n_loc, qstart, m, m_job) = _gen(cfg, rank, world, args.scaling, args.order, "cuda")
     say(f"inputs: {n_loc} keys, {m} queries")
@@ -599,7 +618,8 @@ def main():
         else:
             def e2e_step():
                 bs.bs_lookup_host(idx, hq, m, hout, stream)
-            api = "bs_lookup_host (pinned host buffers)"
+            api = ("bs_lookup_host (pinned host buffers; chunks of 2^22 queries overlap the PCIe copies, "
+                   "each chunk in the in-place mode: the out-of-place reorderings need a caller workspace)")
         e2e_step()   # warm (allocates staging)
         if world > 1:
             torch.distributed.barrier()
@@ -654,6 +674,7 @@ def main():
                    "kary_levels": info["kary_levels"], "kary_smem_levels": info["kary_smem_levels"],
                    "keys_per_gpu": n_loc, "queries_per_gpu": m, "queries_job": m_job,
                    "cache_hints": launch.cache_hints, "kary_mode": launch.kary_mode,
+                   "reorder": REORDER_NAMES.get(launch.reorder, str(launch.reorder)),
                    "parallelism": (f"{mode} x{world}" if world > 1 else "1 GPU"),
                    "l2": ("inputs larger than L2 (queries + results per step > 126 MB), no flush"
                           if m * (kb + ob) > 2 * l2_bytes else "inputs smaller than L2, no flush")},

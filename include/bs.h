@@ -72,14 +72,17 @@ typedef enum {
                               workspace), the segment-staged lookup runs per segment, one pass
                               restores query order.  Needs bs_lookup_ws; n <= 2^26 keys.     */
     BS_REORDER_BUCKET = 5  /* the batch is partitioned by KEY RANGE (P:131-135's global reorder made
-                              coarse): buckets of 2^15 leaves of 32 B (2^17 u64 / 2^18 u32 keys,
-                              an L2-sized slice of the array); one histogram pass, one partition
-                              pass (bucket-major, exact offsets), the per-bucket search (the
-                              bucket's pinned Eytzinger table of leaf maxima staged in shared
-                              memory by TMA, §4.2, then one 32-B leaf, §5), one pass restoring
-                              query order.  Any variant's index (bs_build always builds the
-                              bucket tables, n * key_bytes / 8 bytes, up to 4096 buckets:
-                              n <= 2^29 u64 / 2^30 u32 keys).  Needs bs_lookup_ws.             */
+                              coarse) into buckets whose slice of the array stays L2-resident
+                              while it is searched: a histogram pass, a partition pass
+                              (bucket-major regions, exact offsets), the per-bucket search, one
+                              pass restoring query order.  Fine buckets (n <= 2^27 u64 / 2^28
+                              u32 keys): 2^15 leaves of 32 B, searched through the bucket's
+                              pinned Eytzinger table of leaf maxima staged in shared memory by
+                              TMA (§4.2) and one 32-B leaf (§5).  Coarse buckets (larger n, up
+                              to 2^31 u64 / 2^32 u32 keys): 16-MB key slices searched by the
+                              index's own kernel over the partitioned batch.  Any variant's
+                              index (bs_build always builds the bucket tables: n * key / 8
+                              bytes when fine).  Needs bs_lookup_ws.                         */
 } bs_reorder;
 
 /* Build-time structure + default launch configuration.
@@ -268,7 +271,7 @@ int bs_lookup_host(const void* idx, const void* host_queries, uint64_t m, void* 
  *     launch (NULL = index defaults) needs for m queries (0 if the mode needs
  *     none; BUCKET: m * (key + out + 4) bytes plus per-CTA / per-tile tables).
  *     BS_ERR_UNSUPPORTED if the mode cannot run on this index (GLOBAL:
- *     n > 2^26 keys; BUCKET: more than 4096 buckets; either: m >= 2^32).
+ *     n > 2^26 keys; BUCKET: more than 1024 buckets; either: m >= 2^32).
  *   bs_lookup_ws: bs_lookup_ex plus a caller-owned device workspace `ws` of
  *     ws_bytes (no allocation inside; the workspace must not be shared by calls
  *     in flight on other streams).  BS_ERR_INVALID if ws is NULL / too small for

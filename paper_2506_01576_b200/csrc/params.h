@@ -121,8 +121,9 @@ cudaError_t launch_part_global(int kb, int ob, const void* a, uint64_t n, const 
 // leaves of 32 B, per-bucket pinned Eytzinger tables built by bs_build) are searched
 // by k_bk_search; coarse buckets (arrays too large for <= kBkFineMax fine buckets:
 // slices of kBkCoarseBytes) by the index's own lookup kernel over the partitioned batch.
-constexpr uint32_t kBkMaxBuckets = 4096;    // partition pass keeps per-bucket state in shared memory
-constexpr uint32_t kBkFineMax = 1024;       // most fine buckets (longer runs per tile below this)
+constexpr uint32_t kBkFineMax = 1024;       // most fine buckets (runs per tile long enough to coalesce)
+constexpr uint32_t kBkMaxBuckets = 1024;    // most buckets of either kind (the partition pass keeps two
+                                            // buckets' state per thread in registers)
 constexpr uint64_t kBkCoarseBytes = 16ull << 20;   // coarse bucket slice
 constexpr uint32_t kBkChunk = 16384;        // queries per search item (default)
 struct BucketIndex {

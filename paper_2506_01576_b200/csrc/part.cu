@@ -42,6 +42,9 @@ namespace bs {
 
 constexpr uint32_t kBkTile = 4096;        // queries per partition tile (u16 slots)
 constexpr uint32_t kBkPThreads = 512;     // threads of the streaming passes (hist / part / unpart)
+constexpr uint32_t kBkPCtas = 2;          // their CTAs per SM (tile t on CTA t % (kBkPCtas x SMs));
+                                          // measured: 2048-query tiles on 4 CTAs of 256 threads per SM
+                                          // halve the runs and cost 30 % more DRAM bytes (4.3 ms)
 constexpr uint32_t kBkBinsLog2 = 13;      // radix directory over the 32-bit global image
 constexpr uint32_t kBkBins = 1u << kBkBinsLog2;
 constexpr uint32_t kBkThreads = 1024;        // threads of the search (one CTA per SM)
@@ -170,6 +173,7 @@ struct BkParams {
     K* rq;                   // [m] queries, bucket-major
     void* rp;                // [m] their results, same positions
     uint32_t* bp;            // [m] tile t's sorted position s: bucket | original slot << 16
+    uint16_t* bkid;          // [m] bucket of query j (k_bk_hist -> k_bk_part)
     uint32_t* trun;          // [ntiles * B] (global position of run b) - (its sorted start), mod 2^32
 };
 
@@ -273,7 +277,7 @@ __device__ __forceinline__ uint32_t bk_exscan(uint32_t* v, uint32_t N, uint32_t*
 // ---- pass 1: per-CTA histograms (same tile -> CTA map as k_bk_part); the next
 // tile's queries are in flight while this tile is bucketed
 template <class K>
-__global__ void __launch_bounds__(kBkPThreads, 2)
+__global__ void __launch_bounds__(kBkPThreads, kBkPCtas)
 k_bk_hist(const BkParams<K> p) {
     constexpr uint32_t T = kBkTile, E = T / kBkPThreads;
     extern __shared__ __align__(16) uint32_t sm[];
@@ -304,8 +308,14 @@ k_bk_hist(const BkParams<K> p) {
         for (uint32_t e = 0; e < E; ++e) x[e] = xn[e];
         load_tile(t + gridDim.x, xn);
 #pragma unroll
-        for (uint32_t e = 0; e < E; ++e)
-            if (e * kBkPThreads + threadIdx.x < cntq) atomicAdd(&hist[bk_bucket(p, MS, DIR, x[e])], 1u);
+        for (uint32_t e = 0; e < E; ++e) {
+            const uint32_t j = e * kBkPThreads + threadIdx.x;
+            if (j < cntq) {
+                const uint32_t b = bk_bucket(p, MS, DIR, x[e]);
+                atomicAdd(&hist[b], 1u);
+                __stcs(p.bkid + b0 + j, (uint16_t)b);   // the partition pass reads it back
+            }
+        }
     }
     __syncthreads();
     for (uint32_t b = threadIdx.x; b < p.B; b += blockDim.x) p.cnt[(uint64_t)blockIdx.x * p.B + b] = hist[b];
@@ -345,70 +355,124 @@ k_bk_scan(uint32_t* __restrict__ cnt, uint32_t* __restrict__ tot, uint32_t G, ui
 }
 
 // ---- pass 3: partition (tile t on CTA t % G, as in k_bk_hist)
+//
+// Thread i owns buckets [i BPT, (i+1) BPT) (BPT = ceil(B / threads) <= 2): their
+// tile counts, run starts and global cursors live in its registers, so a tile
+// costs four barriers (ranks / warp totals / run starts / sorted tile) and no
+// loops over the buckets; the next tile's queries and bucket ids are in flight
+// while this tile is sorted and stored.
 template <class K>
-__global__ void __launch_bounds__(kBkPThreads, 2)
+__global__ void __launch_bounds__(kBkPThreads, kBkPCtas)
 k_bk_part(const BkParams<K> p) {
-    constexpr uint32_t T = kBkTile, E = T / kBkPThreads;
+    constexpr uint32_t T = kBkTile, E = T / kBkPThreads, BPT = kBkFineMax / kBkPThreads;
+    constexpr uint32_t NW = kBkPThreads / 32;
     extern __shared__ __align__(16) uint32_t sm[];
-    const uint32_t B = p.B, B4 = (B + 3u) & ~3u;
+    const uint32_t B = p.B;
     K* stq = reinterpret_cast<K*>(sm);                        // [T] queries, bucket order
     uint32_t* sbp = reinterpret_cast<uint32_t*>(stq + T);     // [T] bucket | original slot << 16, bucket order
-    uint32_t* MS = sbp + T;                                   // [B4]
-    uint32_t* hist = MS + B4;                                 // [B4] tile counts
-    uint32_t* loff = hist + B4;                               // [B4] tile run starts (sorted order)
-    uint32_t* cur = loff + B4;                                // [B4] this CTA's next global position per bucket
-    uint32_t* rbase = cur + B4;                               // [B4] global position of run b minus its sorted start
-    uint32_t* tmp = rbase + B4;                               // [64]
-    uint32_t* DIR = tmp + 64;                                 // [kBkBins]
-    bk_stage_dir(p, MS, DIR);
-    // bucket starts (exclusive scan of the bucket sizes) + this CTA's prefix within each bucket
-    for (uint32_t b = threadIdx.x; b < B; b += blockDim.x) { cur[b] = p.tot[b]; hist[b] = 0; }
-    __syncthreads();
-    bk_exscan(cur, B, tmp);
-    for (uint32_t b = threadIdx.x; b < B; b += blockDim.x) cur[b] += p.cnt[(uint64_t)blockIdx.x * B + b];
+    uint32_t* hist = sbp + T;                                 // [kBkFineMax] tile counts (ranks by atomics)
+    uint32_t* loff = hist + kBkFineMax;                       // [kBkFineMax] tile run starts (sorted order)
+    uint32_t* rbase = loff + kBkFineMax;                      // [kBkFineMax] global position of run b minus its sorted start
+    uint32_t* wsum = rbase + kBkFineMax;                      // [NW] warp totals
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t b_lo = threadIdx.x * BPT;
+    // this CTA's next global position per owned bucket: the bucket's start (an
+    // exclusive scan of the bucket sizes) + this CTA's prefix within the bucket
+    uint32_t cur[BPT];
+    {
+        uint32_t own = 0;
+#pragma unroll
+        for (uint32_t k = 0; k < BPT; ++k) {
+            cur[k] = b_lo + k < B ? p.tot[b_lo + k] : 0u;
+            own += cur[k];
+            hist[b_lo + k] = 0;
+        }
+        uint32_t inc = own;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+            if (lane >= (uint32_t)o) inc += y;
+        }
+        if (lane == 31) wsum[warp] = inc;
+        __syncthreads();
+        uint32_t run = inc - own;
+        for (uint32_t w = 0; w < warp; ++w) run += wsum[w];
+#pragma unroll
+        for (uint32_t k = 0; k < BPT; ++k) {
+            const uint32_t c = cur[k];
+            cur[k] = run + (b_lo + k < B ? p.cnt[(uint64_t)blockIdx.x * B + b_lo + k] : 0u);
+            run += c;
+        }
+    }
     const uint64_t pol = p.stream_hint ? policy_evict_first() : policy_evict_normal();
     const uint64_t pol_run = policy_evict_normal();
     const uint64_t ntiles = (p.m + T - 1) / T;
+    K xn[E];
+    uint32_t bn[E];
+    auto load_tile = [&](uint64_t t) {
+        const uint64_t b0 = t * T;
+#pragma unroll
+        for (uint32_t e = 0; e < E; ++e) {
+            const uint64_t j = b0 + e * kBkPThreads + threadIdx.x;
+            const bool ok = t < ntiles && j < p.m;
+            xn[e] = ok ? load_stream(p.q + j, true, pol) : (K)0;
+            bn[e] = ok ? (uint32_t)__ldcs(p.bkid + j) : 0xFFFFu;   // from k_bk_hist
+        }
+    };
+    load_tile(blockIdx.x);
     for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const uint64_t b0 = t * T;
         const uint32_t cntq = (uint32_t)((p.m - b0) < T ? (p.m - b0) : T);
         K x[E];
-        uint32_t bb[E], rr[E];
+        uint32_t br[E];   // bucket | rank in the tile's run << 16
 #pragma unroll
-        for (uint32_t e = 0; e < E; ++e) {
-            const uint32_t j = e * kBkPThreads + threadIdx.x;
-            x[e] = j < cntq ? load_stream(p.q + b0 + j, true, pol) : (K)0;
-        }
-        __syncthreads();   // hist is zero, cur is final, the previous tile's stores are done
+        for (uint32_t e = 0; e < E; ++e) { x[e] = xn[e]; br[e] = bn[e]; }
+        load_tile(t + gridDim.x);
+        __syncthreads();   // (1) hist is zero and the previous tile's readout is done
 #pragma unroll
-        for (uint32_t e = 0; e < E; ++e) {
-            const uint32_t j = e * kBkPThreads + threadIdx.x;
-            bb[e] = 0xFFFFu;
-            if (j < cntq) {
-                bb[e] = bk_bucket(p, MS, DIR, x[e]);
-                rr[e] = atomicAdd(&hist[bb[e]], 1u);
-            }
+        for (uint32_t e = 0; e < E; ++e)
+            if (br[e] != 0xFFFFu) br[e] |= atomicAdd(&hist[br[e]], 1u) << 16;
+        __syncthreads();   // (2) the tile's counts are final
+        uint32_t c[BPT], own = 0;
+#pragma unroll
+        for (uint32_t k = 0; k < BPT; ++k) {
+            c[k] = hist[b_lo + k];
+            hist[b_lo + k] = 0;
+            own += c[k];
         }
-        __syncthreads();
-        for (uint32_t b = threadIdx.x; b < B; b += blockDim.x) loff[b] = hist[b];
-        __syncthreads();
-        bk_exscan(loff, B, tmp);
-        // the run of bucket b starts at cur[b] in the bucket-major array: P3 finds a
-        // sorted position s of bucket b there at (cur[b] - loff[b]) + s
-        for (uint32_t b = threadIdx.x; b < B; b += blockDim.x) {
-            const uint32_t rb = cur[b] - loff[b];
+        uint32_t inc = own;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+            if (lane >= (uint32_t)o) inc += y;
+        }
+        if (lane == 31) wsum[warp] = inc;
+        __syncthreads();   // (3) warp totals
+        uint32_t run = inc - own;
+#pragma unroll
+        for (uint32_t w = 0; w < NW; ++w) run += w < warp ? wsum[w] : 0u;
+#pragma unroll
+        for (uint32_t k = 0; k < BPT; ++k) {
+            // the run of bucket b starts at cur[b] in the bucket-major array: P3 finds a
+            // sorted position s of bucket b there at (cur[b] - loff[b]) + s
+            const uint32_t b = b_lo + k;
+            const uint32_t rb = cur[k] - run;
+            loff[b] = run;
             rbase[b] = rb;
-            p.trun[t * B + b] = rb;
+            if (b < B) p.trun[t * B + b] = rb;
+            cur[k] += c[k];
+            run += c[k];
         }
+        __syncthreads();   // (4) run starts
 #pragma unroll
         for (uint32_t e = 0; e < E; ++e) {
-            if (bb[e] == 0xFFFFu) continue;
-            const uint32_t sidx = loff[bb[e]] + rr[e];
+            if (br[e] == 0xFFFFu) continue;
+            const uint32_t b = br[e] & 0xFFFFu;
+            const uint32_t sidx = loff[b] + (br[e] >> 16);
             stq[sidx] = x[e];
-            sbp[sidx] = bb[e] | ((e * kBkPThreads + threadIdx.x) << 16);
+            sbp[sidx] = b | ((e * kBkPThreads + threadIdx.x) << 16);
         }
-        __syncthreads();
-        for (uint32_t b = threadIdx.x; b < B; b += blockDim.x) { cur[b] += hist[b]; hist[b] = 0; }
+        __syncthreads();   // (5) the sorted tile
         // each run to its place in its bucket's region (consecutive within a run;
         // evict_normal: the run's partial lines are completed by this CTA's next
         // tile and must stay in L2 until then), and the tile's (bucket, slot) list
@@ -428,45 +492,6 @@ k_bk_part(const BkParams<K> p) {
 // exact leaf; the 32-B leaf c then gives lb.  A leaf whose keys are all < q
 // (possible only when a leaf maximum's image ties q's) continues by galloping
 // over the real leaf maxima.
-// the rare image-tie continuation of a leaf scan: the first leaf l > c whose
-// maximum is >= x (galloping over the real leaf maxima), rescanned; returns
-// l | nlt << 32 | eq << 40
-template <class K>
-__device__ __noinline__ uint64_t bk_leaf_tie(const K* __restrict__ ab, uint64_t len, uint32_t Mb, uint32_t c, K x,
-                                             uint64_t pol_leaf) {
-    constexpr uint32_t LK = 32u / sizeof(K);
-    auto mxv = [&](uint32_t j) -> K {
-        const uint64_t e = ((uint64_t)j + 1) * LK;
-        return ldg(ab + (e < len ? e : len) - 1);
-    };
-    uint32_t l = c + 1, step = 1, h;
-    for (;;) {
-        h = l - 1 + step;
-        if (h >= Mb) { h = Mb; break; }
-        if (mxv(h) >= x) break;
-        l = h + 1;
-        step <<= 1;
-    }
-    while (l < h) {
-        const uint32_t mid = (l + h) >> 1;
-        if (mxv(mid) < x) l = mid + 1;
-        else h = mid;
-    }
-    uint32_t nlt = 0;
-    bool eq = false;
-    if (l < Mb) {
-        uint64_t w[4];
-        ld_sector(ab + (uint64_t)l * LK, pol_leaf, w);
-#pragma unroll
-        for (uint32_t u = 0; u < LK; ++u) {
-            const K v = bk_key<K>(w, (int)u);
-            nlt += v < x ? 1u : 0u;
-            eq |= v == x;
-        }
-    }
-    return (uint64_t)l | ((uint64_t)nlt << 32) | ((uint64_t)(eq ? 1u : 0u) << 40);
-}
-
 template <class K, int OB>
 __device__ __forceinline__ void bk_finish(const K* __restrict__ ab, uint64_t klo, uint64_t len, uint32_t Mb,
                                           uint64_t n, K x, uint32_t c, const uint64_t* lv, void* rp, uint32_t ir,
@@ -486,11 +511,39 @@ __device__ __forceinline__ void bk_finish(const K* __restrict__ ab, uint64_t klo
             nlt += v < x ? 1u : 0u;
             eq |= v == x;
         }
-        if (__builtin_expect(nlt == LK && c + 1 < Mb, 0)) {
-            const uint64_t r = bk_leaf_tie<K>(ab, len, Mb, c, x, pol_leaf);
-            c = (uint32_t)r;
-            nlt = (uint32_t)(r >> 32) & 0xFFu;
-            eq = (r >> 40) & 1u;
+        if (nlt == LK && c + 1 < Mb) {
+            // leaf maxima whose image ties q's may still be < q: gallop over the
+            // real maxima to the first >= q, then rescan that leaf
+            auto mxv = [&](uint32_t j) -> K {
+                const uint64_t e = ((uint64_t)j + 1) * LK;
+                return ldg(ab + (e < len ? e : len) - 1);
+            };
+            uint32_t l = c + 1, step = 1, h;
+            for (;;) {
+                h = l - 1 + step;
+                if (h >= Mb) { h = Mb; break; }
+                if (mxv(h) >= x) break;
+                l = h + 1;
+                step <<= 1;
+            }
+            while (l < h) {
+                const uint32_t mid = (l + h) >> 1;
+                if (mxv(mid) < x) l = mid + 1;
+                else h = mid;
+            }
+            c = l;
+            nlt = 0;
+            eq = false;
+            if (l < Mb) {
+                uint64_t w[4];
+                ld_sector(ab + (uint64_t)l * LK, pol_leaf, w);
+#pragma unroll
+                for (uint32_t u = 0; u < LK; ++u) {
+                    const K v = bk_key<K>(w, (int)u);
+                    nlt += v < x ? 1u : 0u;
+                    eq |= v == x;
+                }
+            }
         }
         lb = klo + (uint64_t)c * LK + nlt;
         if (lb > n) lb = n;
@@ -594,7 +647,7 @@ k_bk_search(const BkParams<K> p) {
 
 // ---- pass 5: back to query order (any grid: the run bases are stored per tile)
 template <class K, int OB>
-__global__ void __launch_bounds__(kBkPThreads, 4)
+__global__ void __launch_bounds__(kBkPThreads, 2 * kBkPCtas)
 k_bk_unpart(const BkParams<K> p) {
     using O = typename std::conditional<OB == 8, uint64_t, uint32_t>::type;
     constexpr uint32_t T = kBkTile, E = T / kBkPThreads;
@@ -652,12 +705,12 @@ k_bk_unpart(const BkParams<K> p) {
 
 struct BkLayout {
     uint64_t G, Gs, B, ntiles;
-    uint64_t o_cnt, o_tot, o_rq, o_rp, o_bp, o_trun, total;
+    uint64_t o_cnt, o_tot, o_rq, o_rp, o_bp, o_bkid, o_trun, total;
 };
 
 static bool bk_layout(uint64_t B, uint64_t m, int kb, int ob, uint32_t sm_count, BkLayout* L) {
     if (B == 0 || B > kBkMaxBuckets || m >= (1ull << 32)) return false;
-    L->G = 2ull * sm_count;   // two CTAs of kBkPThreads per SM (hist / part; unpart runs four)
+    L->G = (uint64_t)kBkPCtas * sm_count;   // CTAs of hist / part (unpart runs twice as many)
     L->Gs = sm_count;
     L->B = B;
     L->ntiles = (m + kBkTile - 1) / kBkTile;
@@ -669,6 +722,7 @@ static bool bk_layout(uint64_t B, uint64_t m, int kb, int ob, uint32_t sm_count,
     L->o_rq = take((uint64_t)kb * mm);
     L->o_rp = take((uint64_t)ob * mm);
     L->o_bp = take(4 * mm);
+    L->o_bkid = take(2 * mm);
     L->o_trun = take(4 * L->ntiles * B);
     L->total = o;
     return true;
@@ -704,6 +758,7 @@ static cudaError_t go_bucket(BkParams<K> p, const BkLayout& L, char* ws, cudaStr
     p.rq = (K*)(ws + L.o_rq);
     p.rp = ws + L.o_rp;
     p.bp = (uint32_t*)(ws + L.o_bp);
+    p.bkid = (uint16_t*)(ws + L.o_bkid);
     p.trun = (uint32_t*)(ws + L.o_trun);
     if (run) { run->rq = p.rq; run->rp = p.rp; }
     const uint32_t B = p.B, B4 = (B + 3u) & ~3u;
@@ -717,7 +772,7 @@ static cudaError_t go_bucket(BkParams<K> p, const BkLayout& L, char* ws, cudaStr
         k_bk_scan<<<(B + 31) / 32, 1024, 0, s>>>(p.cnt, p.tot, p.G, B);
         count_launch();
         {
-            const uint32_t smem = kBkTile * ((uint32_t)sizeof(K) + 4u) + 4u * (5u * B4 + 64u) + 4u * kBkBins;
+            const uint32_t smem = kBkTile * ((uint32_t)sizeof(K) + 4u) + 4u * (3u * kBkFineMax + 32u);
             e = bk_launch((const void*)k_bk_part<K>, kBkPThreads, smem, p.G, &p, s);
             if (e != cudaSuccess) return e;
         }
