@@ -18,6 +18,10 @@ KEYS = {   # run name -> (traffic key, queries per launch, kernels of one step)
     "c4": ("config4/random/kary/K5/C16/mode7", 1 << 30, ["k_kary_g1"]),
     "c5": ("config5/random/kary/K5/C16/mode7/peer", 1 << 28, ["k_peer_route", "k_kary_g1", "k_peer_finish"]),
     "c3global": ("config3/random/kary/K5/C16/mode7/r4", 1 << 27, ["k_part", "k_seg_part", "k_part_ovf", "k_unpart"]),
+    "c3bucket": ("config3/random/kary/K5/C16/mode7/r5", 1 << 27,
+                 ["k_bk_hist", "k_bk_scan", "k_bk_part", "k_bk_search", "k_bk_unpart"]),
+    "c4bucket": ("config4/random/kary/K5/C16/mode7/r5", 1 << 30,
+                 ["k_bk_hist", "k_bk_scan", "k_bk_part", "k_kary_g1", "k_bk_unpart"]),
 }
 
 
