@@ -113,7 +113,7 @@ cudaError_t plan_grid(const void* kern, uint32_t threads, uint32_t smem, Grid gr
     return cudaSuccess;
 }
 
-static uint64_t bucket_max_keys(uint32_t kb) { return (uint64_t)kBkMaxBuckets * (kBkCoarseBytes / kb); }
+static uint64_t bucket_max_keys(uint32_t kb) { return (uint64_t)kBkMaxBuckets * ((8ull << 15) * (64u / kb)); }
 
 static bool is_pow2(uint64_t x) { return x && !(x & (x - 1)); }
 
@@ -384,29 +384,36 @@ const char* bs_version(void) {
     return "libbs 0.1 (sm_100a; naive / opt / kary; arXiv 2506.01576)";
 }
 
-// BS_REORDER_BUCKET structures (part.cu).  Fine: buckets of 2^D leaves of 32 B
-// (D = 15; BS_BUCKET_D = 14 for A/B runs) with their pinned tables, while that
-// needs <= kBkFineMax buckets (n <= 2^27 u64 / 2^28 u32 keys); coarse above:
-// buckets of kBkCoarseBytes of keys (searched by the index's own kernel), up to
-// kBkMaxBuckets.  Tables, per-bucket image parameters, bucket maxima and their
-// directory in one allocation.  Not built (the mode reports UNSUPPORTED) above that.
+// BS_REORDER_BUCKET structures (part.cu).  Fine: buckets of 2^D units of one
+// 32-B leaf (D = 15; BS_BUCKET_D = 14 for A/B runs) while that needs <=
+// kBkFineMax buckets (n <= 2^27 u64 / 2^28 u32 keys); above, two-level buckets:
+// 2^15 units of 8 leaves of 64 B (16 MB of keys per bucket) with one 32-B node of
+// leaf-maxima images per unit, up to kBkMaxBuckets (n <= 2^31 u64 / 2^32 u32).
+// Tables, per-bucket image parameters, nodes, bucket maxima and their directory
+// in one allocation.  Not built (the mode reports UNSUPPORTED) above that.
 static int build_bucket_layout(Index* ix, cudaStream_t st, BuildTimer& bt) {
-    uint32_t D = 15;
+    uint32_t D = 15, G = 1;
     if (const char* v = getenv("BS_BUCKET_D")) D = (uint32_t)atoi(v) == 14 ? 14u : 15u;
-    const bool force_coarse = getenv("BS_BUCKET_COARSE") && atoi(getenv("BS_BUCKET_COARSE")) != 0;
+    const bool force_two = getenv("BS_BUCKET_TWO") && atoi(getenv("BS_BUCKET_TWO")) != 0;
     uint64_t NB = (1ull << D) * (32u / ix->kb);
     uint64_t B = (ix->n + NB - 1) / NB;
-    if (B > kBkFineMax || force_coarse) {
-        D = 0;
-        NB = kBkCoarseBytes / ix->kb;
+    uint32_t LB = 32;
+    if (B > kBkFineMax || force_two) {
+        // 64-B leaves (16-MB buckets).  Measured at config 4: 32-B leaves (8-MB
+        // buckets, 1024 of them; BS_BUCKET_LB32=1) ran the search at 25.5 vs 23.0
+        // ms and moved 67 vs 26 DRAM B / lookup
+        D = 15;
+        G = 8;
+        LB = (getenv("BS_BUCKET_LB32") && atoi(getenv("BS_BUCKET_LB32")) != 0) ? 32u : 64u;
+        NB = (8ull << D) * (LB / ix->kb);
         B = (ix->n + NB - 1) / NB;
     }
     if (B > kBkMaxBuckets) return BS_OK;
     cudaError_t e = cudaStreamSynchronize(st);   // a_first / a_last are on the host
     if (e != cudaSuccess) return fail_cuda(e, "bucket tables: sync");
     auto al = [](uint64_t x) { return (x + 255) & ~255ull; };
-    const uint64_t tab_bytes = D ? al(4 * (B << D)) : 0, par_bytes = D ? al(16 * B) : 0;
-    const uint64_t o_tab = 0, o_par = tab_bytes, o_mx = o_par + par_bytes, o_dir = o_mx + al(4 * B);
+    const uint64_t o_tab = 0, o_par = al(4 * (B << D)), o_gn = o_par + al(16 * B);
+    const uint64_t o_mx = o_gn + (G > 1 ? al(4 * (B << D) * G) : 0), o_dir = o_mx + al(4 * B);
     const uint64_t total = o_dir + al(2 * ((1u << 13) + 1));
     e = cudaMalloc(&ix->d_bk, total);
     if (e != cudaSuccess) return fail_cuda(e, "cudaMalloc(bucket tables)");
@@ -415,18 +422,22 @@ static int build_bucket_layout(Index* ix, cudaStream_t st, BuildTimer& bt) {
     bi.B = B;
     bi.NB = NB;
     bi.D = D;
+    bi.G = G;
+    bi.LB = LB;
     bi.gbase = ix->a_first;
     const uint64_t span = ix->a_last - ix->a_first;
     uint32_t bl = 0;
     while (bl < 64 && (span >> bl) != 0) ++bl;
     bi.gsh = bl > 32 ? bl - 32 : 0;
     bt.begin(kStImg);
-    e = build_bucket_index(ix->kb, ix->d_keys, ix->n, D, NB, B, bi.gbase, bi.gsh, D ? (uint32_t*)(p + o_tab) : nullptr,
-                           D ? (uint64_t*)(p + o_par) : nullptr, (uint32_t*)(p + o_mx), (uint16_t*)(p + o_dir), st);
+    e = build_bucket_index(ix->kb, ix->d_keys, ix->n, D, G, LB, NB, B, bi.gbase, bi.gsh, (uint32_t*)(p + o_tab),
+                           (uint64_t*)(p + o_par), G > 1 ? (uint32_t*)(p + o_gn) : nullptr, (uint32_t*)(p + o_mx),
+                           (uint16_t*)(p + o_dir), st);
     bt.end();
     if (e != cudaSuccess) return fail_cuda(e, "build_bucket_index");
-    bi.tab = D ? (const uint32_t*)(p + o_tab) : nullptr;
-    bi.par = D ? (const uint64_t*)(p + o_par) : nullptr;
+    bi.tab = (const uint32_t*)(p + o_tab);
+    bi.par = (const uint64_t*)(p + o_par);
+    bi.gnode = G > 1 ? (const uint32_t*)(p + o_gn) : nullptr;
     bi.mx = (const uint32_t*)(p + o_mx);
     bi.dir = (const uint16_t*)(p + o_dir);
     ix->bk_bytes = total;
@@ -722,15 +733,17 @@ static int lookup_impl(const void* idx, const void* queries, uint64_t m, void* o
         if (const char* v = getenv("BS_BUCKET_CHUNK")) chunk = (uint32_t)atoi(v);
         const uint32_t hint = (L.cache_hints & BS_HINT_STREAM_EVICT_FIRST) ? 1u : 0u;
         cudaStream_t s = (cudaStream_t)stream;
-        if (ix->bk.tab) {   // fine buckets: the whole pipeline in part.cu
+        const char* kv = getenv("BS_BUCKET_KARY");
+        const bool kary_search = kv && atoi(kv) != 0;
+        if (!kary_search) {   // the whole pipeline in part.cu
             cudaError_t e = launch_bucket(ix->kb, ix->ob, ix->bk, ix->d_keys, ix->n, queries, m, out, hint, chunk, ws,
                                           ws_bytes, (uint32_t)ix->sm_count, s, &uns, 0, nullptr);
             if (uns) return fail(BS_ERR_UNSUPPORTED, "BS_REORDER_BUCKET: not supported for this index / batch");
             if (e != cudaSuccess) return fail_cuda(e, "bucket partition launch");
             return BS_OK;
         }
-        // coarse buckets: partition, the index's own kernel over the partitioned
-        // batch (its array accesses now move through one L2-sized slice at a time),
+        // A/B (BS_BUCKET_KARY=1): partition, the index's own kernel over the
+        // partitioned batch (its array accesses move through one slice at a time),
         // then back to query order
         BucketRun run;
         cudaError_t e = launch_bucket(ix->kb, ix->ob, ix->bk, ix->d_keys, ix->n, queries, m, out, hint, chunk, ws,
@@ -743,11 +756,11 @@ static int lookup_impl(const void* idx, const void* queries, uint64_t m, void* o
         // on: leaves must not be marked evict_first (the default for arrays > 2 L2)
         Lk.cache_hints &= ~BS_HINT_LEAF_EVICT_FIRST;
         // one persistent launch over the whole partitioned batch.  Measured
-        // alternatives (config 4): a warp-ticket schedule that keeps every warp
-        // within one chunk of the batch front cut the kernel's DRAM reads from 109
-        // to 17 B / lookup but ran slower (44 vs 39 ms: on L2-hot slices this
-        // kernel is bound by issue and dependent L2 round trips, not DRAM), as did
-        // two lookups per thread (64 ms) and one launch per 2^22 queries
+        // (config 4, 16-MB buckets): 39 ms for this kernel; a warp-ticket schedule
+        // that keeps every warp within one chunk of the batch front cut its DRAM
+        // reads from 109 to 17 B / lookup but ran slower (44 ms: on L2-hot slices
+        // it is bound by issue and dependent L2 round trips), as did two lookups
+        // per thread (64 ms) and one launch per 2^22 queries
         const int rc = dispatch_lookup(ix, run.rq, m, run.rp, s, Lk);
         if (rc != BS_OK) return rc;
         e = launch_bucket(ix->kb, ix->ob, ix->bk, ix->d_keys, ix->n, queries, m, out, hint, chunk, ws, ws_bytes,

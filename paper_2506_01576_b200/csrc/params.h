@@ -117,33 +117,36 @@ cudaError_t launch_part_global(int kb, int ob, const void* a, uint64_t n, const 
                                bool* uns);
 
 // BS_REORDER_BUCKET (part.cu): the batch partitioned by key range into buckets whose
-// slice of the array stays L2-resident while it is searched.  Fine buckets (2^15
-// leaves of 32 B, per-bucket pinned Eytzinger tables built by bs_build) are searched
-// by k_bk_search; coarse buckets (arrays too large for <= kBkFineMax fine buckets:
-// slices of kBkCoarseBytes) by the index's own lookup kernel over the partitioned batch.
-constexpr uint32_t kBkFineMax = 1024;       // most fine buckets (runs per tile long enough to coalesce)
-constexpr uint32_t kBkMaxBuckets = 1024;    // most buckets of either kind (the partition pass keeps two
-                                            // buckets' state per thread in registers)
-constexpr uint64_t kBkCoarseBytes = 16ull << 20;   // coarse bucket slice
+// slice of the array stays L2-resident while it is searched.  Each bucket has a
+// pinned Eytzinger table of 2^D unit maxima images (built by bs_build, staged by
+// TMA).  Fine buckets (n <= 2^27 u64 / 2^28 u32 keys): a unit is one 32-B leaf.
+// Two-level buckets (larger n): a unit is 8 leaves of 64 B (16-MB slices), with a
+// 32-B global node of the 8 leaf maxima images per unit.
+constexpr uint32_t kBkFineMax = 1024;       // most buckets (the partition pass keeps two buckets'
+constexpr uint32_t kBkMaxBuckets = 1024;    // state per thread in registers; runs stay long)
 constexpr uint32_t kBkChunk = 16384;        // queries per search item (default)
 struct BucketIndex {
     uint64_t B = 0;              // buckets
     uint64_t NB = 0;             // keys per bucket (power of two); bucket b = positions [b NB, (b+1) NB)
-    uint32_t D = 0;              // fine: table depth (2^D leaves of 32 B per bucket); 0 = coarse
-    const uint32_t* tab = nullptr;   // fine: [B << D] leaf-maxima images, Eytzinger order per bucket
-    const uint64_t* par = nullptr;   // fine: [2B] per-bucket image base, shift
+    uint32_t D = 0;              // table depth: 2^D units per bucket
+    uint32_t G = 1;              // leaves per unit: 1 (fine) or 8 (two-level)
+    uint32_t LB = 32;            // leaf bytes: 32 (fine), 64 (two-level)
+    const uint32_t* tab = nullptr;   // [B << D] unit-maxima images, Eytzinger order per bucket
+    const uint64_t* par = nullptr;   // [2B] per-bucket image base, shift
+    const uint32_t* gnode = nullptr; // G = 8: [(B << D) * 8] leaf-maxima images in leaf order
     const uint32_t* mx = nullptr;    // [B] bucket-maxima images under the global image
     const uint16_t* dir = nullptr;   // [2^13 + 1] radix directory over mx
     uint64_t gbase = 0;          // global image: min((x - gbase) >> gsh, 2^32 - 1), 0 below gbase
     uint32_t gsh = 0;
 };
 struct BucketRun { void* rq = nullptr; void* rp = nullptr; };   // workspace: partitioned queries, their results
-cudaError_t build_bucket_index(int kb, const void* a, uint64_t n, uint32_t D, uint64_t NB, uint64_t B, uint64_t gbase,
-                               uint32_t gsh, uint32_t* tab, uint64_t* par, uint32_t* mx, uint16_t* dir,
-                               cudaStream_t s);
+cudaError_t build_bucket_index(int kb, const void* a, uint64_t n, uint32_t D, uint32_t G, uint32_t LB, uint64_t NB,
+                               uint64_t B, uint64_t gbase, uint32_t gsh, uint32_t* tab, uint64_t* par, uint32_t* gnode,
+                               uint32_t* mx, uint16_t* dir, cudaStream_t s);
 bool bucket_workspace_bytes(uint64_t B, uint64_t m, int kb, int ob, uint32_t sm_count, uint64_t* bytes);
-// phase 0: the whole fine pipeline; 1: histogram + partition only (run = the partitioned
-// batch, searched by the caller into run->rp); 2: restore query order only
+// phase 0: the whole pipeline; 1: histogram + partition only (run = the partitioned
+// batch, searched by the caller into run->rp: BS_BUCKET_KARY=1 A/B runs); 2: restore
+// query order only
 cudaError_t launch_bucket(int kb, int ob, const BucketIndex& bi, const void* a, uint64_t n, const void* q, uint64_t m,
                           void* out, uint32_t stream_hint, uint32_t chunk, void* ws, uint64_t ws_bytes,
                           uint32_t sm_count, cudaStream_t s, bool* uns, int phase, BucketRun* run);

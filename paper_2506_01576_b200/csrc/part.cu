@@ -129,16 +129,42 @@ __global__ void k_bk_build_dir(const K* __restrict__ a, uint64_t n, uint64_t NB,
     }
 }
 
-cudaError_t build_bucket_index(int kb, const void* a, uint64_t n, uint32_t D, uint64_t NB, uint64_t B, uint64_t gbase,
-                               uint32_t gsh, uint32_t* tab, uint64_t* par, uint32_t* mx, uint16_t* dir,
-                               cudaStream_t s) {
-    const uint32_t LK = 32u / (uint32_t)kb;
+// Two-level buckets (G > 1): per bucket, the images of all its leaf maxima in
+// leaf order (G per table unit, one 32-B node each); leaves past the array:
+// 0xFFFFFFFF.  Uses the bucket parameters written by k_bk_build_tab.
+template <class K>
+__global__ void k_bk_build_gnode(const K* __restrict__ a, uint64_t n, uint32_t D, uint32_t LK, uint32_t G, uint64_t B,
+                                 const uint64_t* __restrict__ par, uint32_t* __restrict__ gnode) {
+    const uint64_t per = (uint64_t)G << D, NB = per * LK;
+    const uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= B * per) return;
+    const uint64_t b = g / per, i = g % per;
+    const uint64_t lo = b * NB, len = (n - lo) < NB ? (n - lo) : NB;
+    uint32_t f = 0xFFFFFFFFu;
+    if (i * LK < len) {
+        const uint64_t e = (i + 1) * LK < len ? (i + 1) * LK : len;
+        f = bk_img((uint64_t)a[lo + e - 1], par[2 * b], (uint32_t)par[2 * b + 1]);
+    }
+    gnode[g] = f;
+}
+
+cudaError_t build_bucket_index(int kb, const void* a, uint64_t n, uint32_t D, uint32_t G, uint32_t LB, uint64_t NB,
+                               uint64_t B, uint64_t gbase, uint32_t gsh, uint32_t* tab, uint64_t* par, uint32_t* gnode,
+                               uint32_t* mx, uint16_t* dir, cudaStream_t s) {
+    const uint32_t LK = LB / (uint32_t)kb;   // keys per leaf
     const uint32_t g2 = (uint32_t)(((B > kBkBins + 1 ? B : kBkBins + 1) + 255) / 256);
     if (tab) {
         const uint64_t tot = B << D;
         const uint32_t g1 = (uint32_t)((tot + 255) / 256);
-        if (kb == 8) k_bk_build_tab<uint64_t><<<g1, 256, 0, s>>>((const uint64_t*)a, n, D, LK, B, tab, par);
-        else k_bk_build_tab<uint32_t><<<g1, 256, 0, s>>>((const uint32_t*)a, n, D, LK, B, tab, par);
+        // table unit = G leaves
+        if (kb == 8) k_bk_build_tab<uint64_t><<<g1, 256, 0, s>>>((const uint64_t*)a, n, D, LK * G, B, tab, par);
+        else k_bk_build_tab<uint32_t><<<g1, 256, 0, s>>>((const uint32_t*)a, n, D, LK * G, B, tab, par);
+        if (G > 1) {
+            const uint64_t tn = (B << D) * G;
+            const uint32_t g3 = (uint32_t)((tn + 255) / 256);
+            if (kb == 8) k_bk_build_gnode<uint64_t><<<g3, 256, 0, s>>>((const uint64_t*)a, n, D, LK, G, B, par, gnode);
+            else k_bk_build_gnode<uint32_t><<<g3, 256, 0, s>>>((const uint32_t*)a, n, D, LK, G, B, par, gnode);
+        }
     }
     if (kb == 8) k_bk_build_dir<uint64_t><<<g2, 256, 0, s>>>((const uint64_t*)a, n, NB, (uint32_t)B, gbase, gsh, mx, dir);
     else k_bk_build_dir<uint32_t><<<g2, 256, 0, s>>>((const uint32_t*)a, n, NB, (uint32_t)B, gbase, gsh, mx, dir);
@@ -155,9 +181,11 @@ struct BkParams {
     uint64_t m;
     void* out;
     uint32_t B;              // buckets
-    uint32_t D;              // per-bucket table depth: 2^D leaves of LK keys per bucket
+    uint32_t D;              // per-bucket table depth: 2^D units per bucket
+    uint32_t LB;             // leaf bytes (32 or 64)
     uint64_t NB;             // keys per bucket = 2^D * LK
-    const uint32_t* tab;     // [B << D] per-bucket Eytzinger tables
+    const uint32_t* tab;     // [B << D] per-bucket Eytzinger tables of unit maxima images
+    const uint32_t* gnode;   // two-level: [(B << D) * 8] leaf maxima images, 8 per unit
     const uint64_t* par;     // [2B] per-bucket image base, shift
     const uint32_t* mx;      // [B] global images of the bucket maxima
     const uint16_t* dir;     // [kBkBins + 1] radix directory over mx
@@ -175,6 +203,7 @@ struct BkParams {
     uint32_t* bp;            // [m] tile t's sorted position s: bucket | original slot << 16
     uint16_t* bkid;          // [m] bucket of query j (k_bk_hist -> k_bk_part)
     uint32_t* trun;          // [ntiles * B] (global position of run b) - (its sorted start), mod 2^32
+    uint32_t* item_ctr;      // search items handed out (zeroed before the search)
 };
 
 // bucket of x: #(bucket maxima < x).  The radix directory packs, per bin of
@@ -488,16 +517,19 @@ k_bk_part(const BkParams<K> p) {
 //
 // One lookup: x's image under the bucket's parameters descends D levels of the
 // staged table (one 4-B shared load per level on the address recurrence
-// a' = 2a - sb + 4 [T[k] < q]), which gives c = #(leaf maxima images < q's) <= the
-// exact leaf; the 32-B leaf c then gives lb.  A leaf whose keys are all < q
-// (possible only when a leaf maximum's image ties q's) continues by galloping
-// over the real leaf maxima.
-template <class K, int OB>
+// a' = 2a - sb + 4 [T[k] < q]), which gives u = #(unit maxima images < q's) <=
+// the exact unit.  Fine buckets (G = 1): a unit is one 32-B leaf.  Two-level
+// buckets (G = 8, arrays above 2^27 u64 keys): a unit is a group of 8 leaves of
+// 64 B, and one 32-B global node of the 8 leaf maxima images (L2-hot) picks the
+// leaf: the next three levels of the same tree, kept in L2.  The leaf gives lb;
+// a leaf whose keys are all < q (possible only when a maximum's image ties q's)
+// continues by galloping over the real leaf maxima.
+template <class K, int OB, int LV>
 __device__ __forceinline__ void bk_finish(const K* __restrict__ ab, uint64_t klo, uint64_t len, uint32_t Mb,
                                           uint64_t n, K x, uint32_t c, const uint64_t* lv, void* rp, uint32_t ir,
                                           uint64_t pol_leaf, uint64_t pol_stream) {
     using O = typename std::conditional<OB == 8, uint64_t, uint32_t>::type;
-    constexpr uint32_t LK = 32u / sizeof(K);
+    constexpr uint32_t LK = 8u * LV / sizeof(K);
     uint64_t lb;
     bool hit = false;
     if (c >= Mb) {
@@ -535,11 +567,8 @@ __device__ __forceinline__ void bk_finish(const K* __restrict__ ab, uint64_t klo
             nlt = 0;
             eq = false;
             if (l < Mb) {
-                uint64_t w[4];
-                ld_sector(ab + (uint64_t)l * LK, pol_leaf, w);
-#pragma unroll
                 for (uint32_t u = 0; u < LK; ++u) {
-                    const K v = bk_key<K>(w, (int)u);
+                    const K v = ldg(ab + (uint64_t)l * LK + u);
                     nlt += v < x ? 1u : 0u;
                     eq |= v == x;
                 }
@@ -553,7 +582,7 @@ __device__ __forceinline__ void bk_finish(const K* __restrict__ ab, uint64_t klo
     store_stream((O*)rp + ir, (O)(hit ? lb : (lb | MISS)), true, pol_stream);
 }
 
-// Items of CH queries in bucket order (CTA c takes items c, c + G, ...: the CTAs
+// Items of CH queries in bucket order, handed out by a global counter (the CTAs
 // work on a window of neighbouring buckets, whose slices of the array stay in
 // L2); the bucket's table is staged once per item that changes bucket.  R
 // lookups per thread descend together (their shared-memory latencies overlap).
@@ -561,11 +590,12 @@ __device__ __forceinline__ void bk_finish(const K* __restrict__ ab, uint64_t klo
 // batch k+1 descends) ran 3 % slower — the kernel is bound by the L1 data pipe
 // (shared-memory bank conflicts of the random probes + one leaf wavefront per
 // lookup), not by latency.
-template <class K, int OB, int D>
+template <class K, int OB, int D, int G, int LV>
 __global__ void __launch_bounds__(kBkThreads, 1)
 k_bk_search(const BkParams<K> p) {
-    constexpr uint32_t LK = 32u / sizeof(K);
-    constexpr uint32_t R = 4;          // lookups in flight per thread
+    // LV: leaf size in u64 words (4: 32 B, 8: 64 B)
+    constexpr uint32_t LK = 8u * LV / sizeof(K);            // keys per leaf
+    constexpr uint32_t R = LV == 4 ? 4 : 2;                 // lookups in flight per thread
     constexpr uint32_t S = 1u << D;
     extern __shared__ __align__(16) uint32_t sm[];
     const uint32_t B = p.B;
@@ -589,7 +619,16 @@ k_bk_search(const BkParams<K> p) {
     const uint32_t sb = smem_u32(Tab);
     const uint32_t step_lt = 4u - sb, step_ge = 0u - sb;
     uint32_t staged = 0xFFFFFFFFu;
-    for (uint32_t it = blockIdx.x; it < I; it += gridDim.x) {
+    // items in bucket order from a global counter: every CTA stays within one
+    // item of the front, so the CTAs work on a window of neighbouring buckets
+    // for the whole batch (a static item stride lets them drift apart)
+    uint32_t* s_it = tmp + 48;
+    for (;;) {
+        __syncthreads();   // s_it free; every lookup of the previous item is issued
+        if (threadIdx.x == 0) *s_it = atomicAdd(p.item_ctr, 1u);
+        __syncthreads();
+        const uint32_t it = *s_it;
+        if (it >= I) break;
         // bucket of item it: the last b with ipre[b] <= it (it has items, so ipre[b+1] > it)
         uint32_t lo = 0, hi = B;
         while (hi - lo > 1) {
@@ -609,8 +648,9 @@ k_bk_search(const BkParams<K> p) {
         const uint32_t sh = (uint32_t)p.par[2 * b + 1];
         const uint64_t klo = (uint64_t)b * p.NB;
         const uint64_t len = (p.n - klo) < p.NB ? (p.n - klo) : p.NB;
-        const uint32_t Mb = (uint32_t)((len + LK - 1) / LK);
+        const uint32_t Mb = (uint32_t)((len + LK - 1) / LK);   // leaves holding keys
         const K* ab = p.a + klo;
+        const uint32_t* gn = p.gnode + ((uint64_t)b << D) * G;  // G = 8: leaf maxima images, 8 per unit
         for (uint32_t i = i0 + threadIdx.x; i < i1; i += kBkThreads * R) {
             K x[R];
             uint32_t ad[R], fq[R];
@@ -629,17 +669,38 @@ k_bk_search(const BkParams<K> p) {
                     ad[r] = 2u * ad[r] + (h < fq[r] ? step_lt : step_ge);
                 }
             }
-            uint64_t lv[R][4];
             uint32_t c[R];
 #pragma unroll
+            for (uint32_t r = 0; r < R; ++r) c[r] = ((ad[r] - sb) >> 2) - S;   // unit
+            if constexpr (G > 1) {
+                // the unit's node of G leaf maxima images (32 B, one sector): leaf = G u + #(< q)
+                uint64_t nd[R][4];
+#pragma unroll
+                for (uint32_t r = 0; r < R; ++r)
+                    if (c[r] * G < Mb) ld_sector(gn + (uint64_t)c[r] * G, pol_leaf, nd[r]);
+#pragma unroll
+                for (uint32_t r = 0; r < R; ++r) {
+                    uint32_t j = 0;
+#pragma unroll
+                    for (uint32_t k = 0; k < 8; ++k) {
+                        const uint32_t im = (uint32_t)(nd[r][k >> 1] >> (32 * (k & 1)));
+                        j += im < fq[r] ? 1u : 0u;
+                    }
+                    c[r] = c[r] * G < Mb ? c[r] * G + j : Mb;
+                }
+            }
+            uint64_t lv[R][LV];
+#pragma unroll
             for (uint32_t r = 0; r < R; ++r) {
-                c[r] = ((ad[r] - sb) >> 2) - S;
-                if (c[r] < Mb) ld_sector(ab + (uint64_t)c[r] * LK, pol_leaf, lv[r]);
+                if (c[r] < Mb) {
+#pragma unroll
+                    for (uint32_t h = 0; h < LV; h += 4) ld_sector(ab + (uint64_t)c[r] * LK + h * (8 / sizeof(K)), pol_leaf, &lv[r][h]);
+                }
             }
 #pragma unroll
             for (uint32_t r = 0; r < R; ++r) {
                 const uint32_t ir = i + r * kBkThreads;
-                if (ir < i1) bk_finish<K, OB>(ab, klo, len, Mb, p.n, x[r], c[r], lv[r], p.rp, ir, pol_leaf, pol_stream);
+                if (ir < i1) bk_finish<K, OB, LV>(ab, klo, len, Mb, p.n, x[r], c[r], lv[r], p.rp, ir, pol_leaf, pol_stream);
             }
         }
     }
@@ -705,7 +766,7 @@ k_bk_unpart(const BkParams<K> p) {
 
 struct BkLayout {
     uint64_t G, Gs, B, ntiles;
-    uint64_t o_cnt, o_tot, o_rq, o_rp, o_bp, o_bkid, o_trun, total;
+    uint64_t o_cnt, o_tot, o_rq, o_rp, o_bp, o_bkid, o_trun, o_ctr, total;
 };
 
 static bool bk_layout(uint64_t B, uint64_t m, int kb, int ob, uint32_t sm_count, BkLayout* L) {
@@ -724,6 +785,7 @@ static bool bk_layout(uint64_t B, uint64_t m, int kb, int ob, uint32_t sm_count,
     L->o_bp = take(4 * mm);
     L->o_bkid = take(2 * mm);
     L->o_trun = take(4 * L->ntiles * B);
+    L->o_ctr = take(4);
     L->total = o;
     return true;
 }
@@ -760,6 +822,7 @@ static cudaError_t go_bucket(BkParams<K> p, const BkLayout& L, char* ws, cudaStr
     p.bp = (uint32_t*)(ws + L.o_bp);
     p.bkid = (uint16_t*)(ws + L.o_bkid);
     p.trun = (uint32_t*)(ws + L.o_trun);
+    p.item_ctr = (uint32_t*)(ws + L.o_ctr);
     if (run) { run->rq = p.rq; run->rp = p.rp; }
     const uint32_t B = p.B, B4 = (B + 3u) & ~3u;
     cudaError_t e;
@@ -779,9 +842,14 @@ static cudaError_t go_bucket(BkParams<K> p, const BkLayout& L, char* ws, cudaStr
     }
     if (phase == 0) {
         const uint32_t smem = (4u << p.D) + 8u * ((B + 4u) & ~3u) + 4u * 64u + 16u;
-        const void* kern = p.D == 15 ? (const void*)k_bk_search<K, OB, 15>
-                         : p.D == 14 ? (const void*)k_bk_search<K, OB, 14> : nullptr;
+        const void* kern = nullptr;
+        if (p.gnode && p.D == 15) kern = p.LB == 32 ? (const void*)k_bk_search<K, OB, 15, 8, 4>
+                                                    : (const void*)k_bk_search<K, OB, 15, 8, 8>;
+        else if (!p.gnode) kern = p.D == 15 ? (const void*)k_bk_search<K, OB, 15, 1, 4>
+                                : p.D == 14 ? (const void*)k_bk_search<K, OB, 14, 1, 4> : nullptr;
         if (!kern) return cudaErrorInvalidValue;
+        e = cudaMemsetAsync(p.item_ctr, 0, sizeof(uint32_t), s);
+        if (e != cudaSuccess) return e;
         e = bk_launch(kern, kBkThreads, smem, p.Gs, &p, s);
         if (e != cudaSuccess) return e;
     }
@@ -803,8 +871,8 @@ cudaError_t launch_bucket(int kb, int ob, const BucketIndex& bi, const void* a, 
     }
     auto fill = [&](auto& p) {
         p.n = n; p.m = m; p.out = out; p.stream_hint = stream_hint;
-        p.B = (uint32_t)bi.B; p.D = bi.D; p.NB = bi.NB;
-        p.tab = bi.tab; p.par = bi.par; p.mx = bi.mx; p.dir = bi.dir;
+        p.B = (uint32_t)bi.B; p.D = bi.D; p.NB = bi.NB; p.LB = bi.LB;
+        p.tab = bi.tab; p.par = bi.par; p.mx = bi.mx; p.dir = bi.dir; p.gnode = bi.gnode;
         p.gbase = bi.gbase; p.gsh = bi.gsh;
         p.CH = chunk ? chunk : kBkChunk;
     };

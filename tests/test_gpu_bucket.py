@@ -142,21 +142,56 @@ def test_bucket_config3_sample():
     idx.close()
 
 
-# ------------------------------------------------------------------ coarse buckets (large arrays)
+# ------------------------------------------------------------------ two-level buckets (large arrays)
 
 @pytest.mark.parametrize("kb", [4, 8])
 @pytest.mark.parametrize("variant", [bs.KARY, bs.OPT, bs.NAIVE])
-def test_bucket_coarse(kb, variant, monkeypatch):
-    """Coarse buckets (slices of 16 MB of keys, searched by the index's own kernel
-    over the partitioned batch) — the layout bs_build picks for arrays above 2^27
-    u64 / 2^28 u32 keys; forced here with BS_BUCKET_COARSE=1 on arrays of a few slices."""
-    monkeypatch.setenv("BS_BUCKET_COARSE", "1")
+def test_bucket_two_level(kb, variant, monkeypatch):
+    """Two-level buckets (2^15 units of 8 leaves of 64 B, or of 32 B with the A/B
+    knob BS_BUCKET_LB32=1, a 32-B node of leaf-maxima images per unit) — the layout bs_build picks above 2^27 u64 / 2^28 u32 keys;
+    forced here with BS_BUCKET_TWO=1 on arrays of a few buckets.  Also the A/B
+    path that searches the partitioned batch with the index's own kernel
+    (BS_BUCKET_KARY=1)."""
+    monkeypatch.setenv("BS_BUCKET_TWO", "1")
     per = (16 << 20) // kb
     n = 2 * per + 12345
     keys = workload.gen_keys(n, kb, seed=900 + kb + variant)
     for order in ("random", "sorted"):
         q = queries_for(keys, 150000, 901, order)
         for ob in ((4, 8) if kb == 4 else (8,)):
-            idx = build(keys, variant=variant, out_bytes=ob)
-            check(bk_run(idx, q, ob), oracle.lookup(keys, q, out_bytes=ob), q, f"coarse kb={kb} v={variant} {order} ob={ob}")
-            idx.close()
+            want = oracle.lookup(keys, q, out_bytes=ob)
+            for lb32 in ("0", "1"):
+                monkeypatch.setenv("BS_BUCKET_LB32", lb32)
+                idx = build(keys, variant=variant, out_bytes=ob)
+                check(bk_run(idx, q, ob), want, q, f"two-level kb={kb} v={variant} {order} ob={ob} lb32={lb32}")
+                monkeypatch.setenv("BS_BUCKET_KARY", "1")
+                check(bk_run(idx, q, ob), want, q, f"partitioned own-kernel kb={kb} v={variant} {order} ob={ob}")
+                monkeypatch.delenv("BS_BUCKET_KARY")
+                idx.close()
+
+
+@pytest.mark.parametrize("kind", ["dups", "clustered", "top"])
+def test_bucket_two_level_distributions(kind, monkeypatch):
+    """Image ties at the node level (clustered keys in a wide span), duplicate
+    runs across leaves / units / buckets, MAX keys — two-level buckets."""
+    monkeypatch.setenv("BS_BUCKET_TWO", "1")
+    rng = np.random.default_rng({"dups": 31, "clustered": 32, "top": 33}[kind])
+    per = 1 << 21
+    n = 2 * per + 777
+    if kind == "dups":
+        v = np.repeat(rng.integers(0, 1 << 62, size=n // 100, dtype=np.uint64), 100)
+        v = np.concatenate([v, np.full(per + 5, 1 << 61, dtype=np.uint64)])
+    elif kind == "clustered":
+        v = np.concatenate([rng.integers(0, 1 << 16, size=n // 2, dtype=np.uint64),
+                            rng.integers(0, 1 << 63, size=n // 2, dtype=np.uint64) * np.uint64(2)])
+    else:
+        v = np.concatenate([np.full(per // 2, (1 << 64) - 1, dtype=np.uint64),
+                            rng.integers((1 << 64) - (1 << 44), (1 << 64) - 1, size=n, dtype=np.uint64)])
+    keys = np.sort(v)
+    q = queries_for(keys, 200000, 34, "random")
+    want = oracle.lookup(keys, q, out_bytes=8)
+    for lb32 in ("0", "1"):
+        monkeypatch.setenv("BS_BUCKET_LB32", lb32)
+        idx = build(keys, variant=bs.KARY, out_bytes=8)
+        check(bk_run(idx, q, 8), want, q, f"two-level {kind} lb32={lb32}")
+        idx.close()
