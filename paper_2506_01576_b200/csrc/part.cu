@@ -40,9 +40,9 @@
 
 namespace bs {
 
-constexpr uint32_t kBkTile = 4096;        // queries per partition tile (u16 slots)
-constexpr uint32_t kBkPThreads = 512;     // threads of the streaming passes (hist / part / unpart)
-constexpr uint32_t kBkPCtas = 2;          // their CTAs per SM (tile t on CTA t % (kBkPCtas x SMs));
+constexpr uint32_t kBkTile = 8192;        // queries per partition tile (u16 slots)
+constexpr uint32_t kBkPThreads = 1024;    // threads of the streaming passes (hist / part / unpart)
+constexpr uint32_t kBkPCtas = 1;          // their CTAs per SM (tile t on CTA t % (kBkPCtas x SMs));
                                           // measured: 2048-query tiles on 4 CTAs of 256 threads per SM
                                           // halve the runs and cost 30 % more DRAM bytes (4.3 ms)
 constexpr uint32_t kBkBinsLog2 = 13;      // radix directory over the 32-bit global image

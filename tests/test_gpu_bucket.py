@@ -19,7 +19,7 @@ from paper_2506_01576_b200 import bs  # noqa: E402
 from test_gpu_parity import build, check  # noqa: E402
 
 NB = {8: 1 << 17, 4: 1 << 18}   # keys per bucket (part.cu: 2^15 leaves of 32 B)
-T = 4096                          # queries per partition tile
+T = 8192                          # queries per partition tile
 
 
 def bk_run(idx, q, ob):
