@@ -40,8 +40,10 @@
 
 namespace bs {
 
-constexpr uint32_t kBkTile = 8192;        // queries per partition tile (u16 slots)
+constexpr uint32_t kBkTile = 8192;        // queries per partition tile (u16 slots); measured: 4096 (2 CTAs of
+                                          // 512 threads per SM) 3.30 ms, 8192 3.08 ms, 16384 3.19 ms at config 3
 constexpr uint32_t kBkPThreads = 1024;    // threads of the streaming passes (hist / part / unpart)
+constexpr uint32_t kBkUCtas = kBkTile * 8u <= (96u << 10) ? 2u : 1u;   // unpartition CTAs per SM
 constexpr uint32_t kBkPCtas = 1;          // their CTAs per SM (tile t on CTA t % (kBkPCtas x SMs));
                                           // measured: 2048-query tiles on 4 CTAs of 256 threads per SM
                                           // halve the runs and cost 30 % more DRAM bytes (4.3 ms)
@@ -327,15 +329,20 @@ k_bk_hist(const BkParams<K> p) {
             xs[e] = (t < ntiles && j < p.m) ? load_stream(p.q + j, true, pol) : (K)0;
         }
     };
-    K xn[E];
-    load_tile(blockIdx.x, xn);
+    constexpr bool PF = E <= 8;   // the next tile in flight when the registers allow it
+    K xn[PF ? E : 1];
+    if constexpr (PF) load_tile(blockIdx.x, xn);
     for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const uint64_t b0 = t * T;
         const uint32_t cntq = (uint32_t)((p.m - b0) < T ? (p.m - b0) : T);
         K x[E];
+        if constexpr (PF) {
 #pragma unroll
-        for (uint32_t e = 0; e < E; ++e) x[e] = xn[e];
-        load_tile(t + gridDim.x, xn);
+            for (uint32_t e = 0; e < E; ++e) x[e] = xn[e];
+            load_tile(t + gridDim.x, xn);
+        } else {
+            load_tile(t, x);
+        }
 #pragma unroll
         for (uint32_t e = 0; e < E; ++e) {
             const uint32_t j = e * kBkPThreads + threadIdx.x;
@@ -436,27 +443,32 @@ k_bk_part(const BkParams<K> p) {
     const uint64_t pol = p.stream_hint ? policy_evict_first() : policy_evict_normal();
     const uint64_t pol_run = policy_evict_normal();
     const uint64_t ntiles = (p.m + T - 1) / T;
-    K xn[E];
-    uint32_t bn[E];
-    auto load_tile = [&](uint64_t t) {
+    constexpr bool PF = E <= 8;   // the next tile in flight when the registers allow it
+    K xn[PF ? E : 1];
+    uint32_t bn[PF ? E : 1];
+    auto load_tile = [&](uint64_t t, K* xs, uint32_t* bs) {
         const uint64_t b0 = t * T;
 #pragma unroll
         for (uint32_t e = 0; e < E; ++e) {
             const uint64_t j = b0 + e * kBkPThreads + threadIdx.x;
             const bool ok = t < ntiles && j < p.m;
-            xn[e] = ok ? load_stream(p.q + j, true, pol) : (K)0;
-            bn[e] = ok ? (uint32_t)__ldcs(p.bkid + j) : 0xFFFFu;   // from k_bk_hist
+            xs[e] = ok ? load_stream(p.q + j, true, pol) : (K)0;
+            bs[e] = ok ? (uint32_t)__ldcs(p.bkid + j) : 0xFFFFu;   // from k_bk_hist
         }
     };
-    load_tile(blockIdx.x);
+    if constexpr (PF) load_tile(blockIdx.x, xn, bn);
     for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const uint64_t b0 = t * T;
         const uint32_t cntq = (uint32_t)((p.m - b0) < T ? (p.m - b0) : T);
         K x[E];
         uint32_t br[E];   // bucket | rank in the tile's run << 16
+        if constexpr (PF) {
 #pragma unroll
-        for (uint32_t e = 0; e < E; ++e) { x[e] = xn[e]; br[e] = bn[e]; }
-        load_tile(t + gridDim.x);
+            for (uint32_t e = 0; e < E; ++e) { x[e] = xn[e]; br[e] = bn[e]; }
+            load_tile(t + gridDim.x, xn, bn);
+        } else {
+            load_tile(t, x, br);
+        }
         __syncthreads();   // (1) hist is zero and the previous tile's readout is done
 #pragma unroll
         for (uint32_t e = 0; e < E; ++e)
@@ -708,7 +720,7 @@ k_bk_search(const BkParams<K> p) {
 
 // ---- pass 5: back to query order (any grid: the run bases are stored per tile)
 template <class K, int OB>
-__global__ void __launch_bounds__(kBkPThreads, 2 * kBkPCtas)
+__global__ void __launch_bounds__(kBkPThreads, kBkUCtas)
 k_bk_unpart(const BkParams<K> p) {
     using O = typename std::conditional<OB == 8, uint64_t, uint32_t>::type;
     constexpr uint32_t T = kBkTile, E = T / kBkPThreads;
@@ -855,7 +867,7 @@ static cudaError_t go_bucket(BkParams<K> p, const BkLayout& L, char* ws, cudaStr
     }
     if (phase != 1) {
         const uint32_t smem = kBkTile * OB + 4u * B4;
-        e = bk_launch((const void*)k_bk_unpart<K, OB>, kBkPThreads, smem, 2u * p.G, &p, s);
+        e = bk_launch((const void*)k_bk_unpart<K, OB>, kBkPThreads, smem, kBkUCtas * p.Gs, &p, s);
         if (e != cudaSuccess) return e;
     }
     return cudaGetLastError();
