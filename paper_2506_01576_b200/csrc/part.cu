@@ -489,9 +489,14 @@ k_bk_part(const BkParams<K> p) {
         }
         if (lane == 31) wsum[warp] = inc;
         __syncthreads();   // (3) warp totals
-        uint32_t run = inc - own;
+        // this warp's offset: exclusive scan of the warp totals across the lanes
+        uint32_t ws = lane < NW ? wsum[lane] : 0u, wi = ws;
 #pragma unroll
-        for (uint32_t w = 0; w < NW; ++w) run += w < warp ? wsum[w] : 0u;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, wi, o);
+            if (lane >= (uint32_t)o) wi += y;
+        }
+        uint32_t run = inc - own + __shfl_sync(0xFFFFFFFFu, wi - ws, warp);
 #pragma unroll
         for (uint32_t k = 0; k < BPT; ++k) {
             // the run of bucket b starts at cur[b] in the bucket-major array: P3 finds a
