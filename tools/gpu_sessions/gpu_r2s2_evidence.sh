@@ -27,6 +27,7 @@ run() {  # name, args
 }
 run c3bucket --steps 1 --warmup 3 --no-e2e --no-naive
 run c4bucket --config config4 --steps 1 --warmup 3 --no-e2e --no-naive
+run c5 --config config5 --steps 1 --warmup 3 --no-e2e --no-dist
 CMD="python bench.py --steps 3 --warmup 3 --no-e2e --no-naive"
 $CMD > $O/plain_launch.log 2>&1 && timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv $CMD > $O/ncu_launches.log 2>&1; echo "launch rc=$?"
 CMD="python bench.py --steps 1 --warmup 3 --no-e2e --no-naive"

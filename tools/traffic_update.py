@@ -21,7 +21,7 @@ KEYS = {   # run name -> (traffic key, queries per launch, kernels of one step)
     "c3bucket": ("config3/random/kary/K5/C16/mode7/r5", 1 << 27,
                  ["k_bk_hist", "k_bk_scan", "k_bk_part", "k_bk_search", "k_bk_unpart"]),
     "c4bucket": ("config4/random/kary/K5/C16/mode7/r5", 1 << 30,
-                 ["k_bk_hist", "k_bk_scan", "k_bk_part", "k_kary_g1", "k_bk_unpart"]),
+                 ["k_bk_hist", "k_bk_scan", "k_bk_part", "k_bk_search", "k_bk_unpart"]),
 }
 
 
