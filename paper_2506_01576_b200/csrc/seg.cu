@@ -113,15 +113,12 @@ __device__ __forceinline__ void stage_segment(uint32_t* F, const K* __restrict__
     }
 }
 
-// lb - (segment start) and the hit flag of an in-range query x
+// lb - (segment start) and the hit flag of an in-range query x, from the
+// node k (in [S, 2S)) its descent of the D image levels reached
 template <class K, int D>
-__device__ __forceinline__ uint32_t seg_search(const uint32_t* F, const K* __restrict__ seg, uint32_t len, K smin,
-                                               uint32_t sh, K x, bool* hit) {
+__device__ __forceinline__ uint32_t seg_finish(const uint32_t* F, const K* __restrict__ seg, uint32_t len, K smin,
+                                               uint32_t sh, K x, uint32_t k, bool* hit) {
     constexpr uint32_t S = 1u << D;
-    const uint32_t fx = seg_image(x, smin, sh);
-    uint32_t k = 1;
-#pragma unroll
-    for (int d = 0; d < D; ++d) k = 2u * k + (F[k] < fx ? 1u : 0u);
     uint32_t c = k - S;                  // keys whose image is below q's: <= lb - seg start
     K v;
     if (sh == 0) {
@@ -155,6 +152,16 @@ __device__ __forceinline__ uint32_t seg_search(const uint32_t* F, const K* __res
     return c;
 }
 
+template <class K, int D>
+__device__ __forceinline__ uint32_t seg_search(const uint32_t* F, const K* __restrict__ seg, uint32_t len, K smin,
+                                               uint32_t sh, K x, bool* hit) {
+    const uint32_t fx = seg_image(x, smin, sh);
+    uint32_t k = 1;
+#pragma unroll
+    for (int d = 0; d < D; ++d) k = 2u * k + (F[k] < fx ? 1u : 0u);
+    return seg_finish<K, D>(F, seg, len, smin, sh, x, k, hit);
+}
+
 template <int OB>
 __device__ __forceinline__ uint64_t enc(uint64_t lb, bool hit) {
     constexpr uint64_t MISS = 1ull << (8 * OB - 1);
@@ -177,31 +184,74 @@ k_seg_sorted(const SegParams<K> p) {
         const uint64_t b = b0 + i;
         bnd[i] = b == 0 ? 0 : b >= B ? m : upper_bound_any(p.q, m, ldg(p.a + b * S - 1));
     }
+    // the next segment's keys are in flight (registers) while this segment is
+    // searched; each thread carries R lookups through the image levels together
+    constexpr uint32_t KPT = S / 1024;   // keys per thread (blockDim 1024)
+    constexpr uint32_t R = 4;
+    K nk[KPT];
+    auto load_keys = [&](uint64_t b) {
+        const uint64_t lo = b * S;
+        const uint32_t len = b < b1 ? (uint32_t)((n - lo) < S ? (n - lo) : S) : 0u;
+#pragma unroll
+        for (uint32_t k = 0; k < KPT; ++k) {
+            const uint32_t i = k * 1024u + threadIdx.x;
+            nk[k] = i < len ? ldg(p.a + lo + i) : (K)0;
+        }
+    };
+    load_keys(b0);
     for (uint64_t b = b0; b < b1; ++b) {
         const uint64_t lo = b * S;
         const uint32_t len = (uint32_t)((n - lo) < S ? (n - lo) : S);
         const K* seg = p.a + lo;
         const K smin = ldg(seg), smax = ldg(seg + len - 1);
         const uint32_t sh = image_shift(smin, smax);
+        K kk[KPT];
+#pragma unroll
+        for (uint32_t k = 0; k < KPT; ++k) kk[k] = nk[k];
+        load_keys(b + 1);
         __syncthreads();   // previous segment's searches are done with F (and bnd is written)
-        stage_segment<K, D>(F, seg, len, smin, sh);
+#pragma unroll
+        for (uint32_t k = 0; k < KPT; ++k) {
+            const uint32_t i = k * 1024u + threadIdx.x;
+            const uint32_t f = i < len ? seg_image(kk[k], smin, sh) : 0xFFFFFFFFu;
+            F[i == S - 1 ? 0u : eytz_slot<D>(i)] = f;
+        }
         __syncthreads();
         const K lower = b ? ldg(p.a + lo - 1) : (K)0;
         const bool first = b == 0, last = b == B - 1;
         const uint64_t q0 = bnd[b - b0], q1 = bnd[b - b0 + 1];
-        for (uint64_t i = q0 + threadIdx.x; i < q1; i += blockDim.x) {
-            const K x = load_stream(p.q + i, true, pol_stream);
-            uint64_t lb;
-            bool hit;
-            if ((first || x > lower) && (last || x <= smax)) {
-                lb = lo + seg_search<K, D>(F, seg, len, smin, sh, x, &hit);
-            } else {
-                lb = lower_bound_global(p.a, n, x);
-                hit = lb < n && ldg(p.a + lb) == x;
+        for (uint64_t i = q0 + threadIdx.x; i < q1; i += 1024u * R) {
+            K x[R];
+            uint32_t fx[R], kq[R];
+#pragma unroll
+            for (uint32_t r = 0; r < R; ++r) {
+                const uint64_t ir = i + r * 1024u;
+                x[r] = ir < q1 ? load_stream(p.q + ir, true, pol_stream) : smin;
+                fx[r] = seg_image(x[r], smin, sh);
+                kq[r] = 1;
             }
-            const uint64_t r = enc<OB>(lb, hit);
-            if constexpr (OB == 8) store_stream((uint64_t*)p.out + i, r, true, pol_stream);
-            else store_stream((uint32_t*)p.out + i, (uint32_t)r, true, pol_stream);
+#pragma unroll
+            for (int d = 0; d < D; ++d) {
+#pragma unroll
+                for (uint32_t r = 0; r < R; ++r) kq[r] = 2u * kq[r] + (F[kq[r]] < fx[r] ? 1u : 0u);
+            }
+#pragma unroll
+            for (uint32_t r = 0; r < R; ++r) {
+                const uint64_t ir = i + r * 1024u;
+                if (ir >= q1) continue;
+                uint64_t lb;
+                bool hit;
+                if ((first || x[r] > lower) && (last || x[r] <= smax)) {
+                    lb = lo + seg_finish<K, D>(F, seg, len, smin, sh, x[r], kq[r], &hit);
+                } else {
+                    // outside the segment's key range (an unsorted batch): plain bisection
+                    lb = lower_bound_global(p.a, n, x[r]);
+                    hit = lb < n && ldg(p.a + lb) == x[r];
+                }
+                const uint64_t res = enc<OB>(lb, hit);
+                if constexpr (OB == 8) store_stream((uint64_t*)p.out + ir, res, true, pol_stream);
+                else store_stream((uint32_t*)p.out + ir, (uint32_t)res, true, pol_stream);
+            }
         }
     }
 }
