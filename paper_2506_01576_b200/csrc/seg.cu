@@ -220,6 +220,9 @@ k_seg_sorted(const SegParams<K> p) {
         const K lower = b ? ldg(p.a + lo - 1) : (K)0;
         const bool first = b == 0, last = b == B - 1;
         const uint64_t q0 = bnd[b - b0], q1 = bnd[b - b0 + 1];
+        // the descent runs on the shared address a = sb + 4k: a' = 2a - sb + 4 [F[k] < q]
+        const uint32_t sb = smem_u32(F);
+        const uint32_t step_lt = 4u - sb, step_ge = 0u - sb;
         for (uint64_t i = q0 + threadIdx.x; i < q1; i += 1024u * R) {
             K x[R];
             uint32_t fx[R], kq[R];
@@ -228,13 +231,18 @@ k_seg_sorted(const SegParams<K> p) {
                 const uint64_t ir = i + r * 1024u;
                 x[r] = ir < q1 ? load_stream(p.q + ir, true, pol_stream) : smin;
                 fx[r] = seg_image(x[r], smin, sh);
-                kq[r] = 1;
+                kq[r] = sb + 4u;
             }
 #pragma unroll
             for (int d = 0; d < D; ++d) {
 #pragma unroll
-                for (uint32_t r = 0; r < R; ++r) kq[r] = 2u * kq[r] + (F[kq[r]] < fx[r] ? 1u : 0u);
+                for (uint32_t r = 0; r < R; ++r) {
+                    const uint32_t h = lds_u32(kq[r]);
+                    kq[r] = 2u * kq[r] + (h < fx[r] ? step_lt : step_ge);
+                }
             }
+#pragma unroll
+            for (uint32_t r = 0; r < R; ++r) kq[r] = (kq[r] - sb) >> 2;
 #pragma unroll
             for (uint32_t r = 0; r < R; ++r) {
                 const uint64_t ir = i + r * 1024u;
