@@ -115,10 +115,12 @@ __device__ __forceinline__ void stage_segment(uint32_t* F, const K* __restrict__
 
 // lb - (segment start) and the hit flag of an in-range query x, from the
 // node k (in [S, 2S)) its descent of the D image levels reached
-template <class K, int D>
+// SMEM: seg points to shared memory (the staged keys), read with plain loads
+template <class K, int D, bool SMEM = false>
 __device__ __forceinline__ uint32_t seg_finish(const uint32_t* F, const K* __restrict__ seg, uint32_t len, K smin,
                                                uint32_t sh, K x, uint32_t k, bool* hit) {
     constexpr uint32_t S = 1u << D;
+    auto rd = [&](uint32_t i) -> K { if constexpr (SMEM) return seg[i]; else return ldg(seg + i); };
     uint32_t c = k - S;                  // keys whose image is below q's: <= lb - seg start
     K v;
     if (sh == 0) {
@@ -128,24 +130,24 @@ __device__ __forceinline__ uint32_t seg_finish(const uint32_t* F, const K* __res
         // the last segment's queries above every key
         if (c < len && v < x) c = len;
     } else {
-        v = c < len ? ldg(seg + c) : (K)0;
+        v = c < len ? rd(c) : (K)0;
         if (c < len && v < x) {
             // keys sharing q's image: gallop, then bisect (seg[c] < x)
             uint32_t l = c + 1, step = 1, h;
             for (;;) {
                 h = l - 1 + step;
                 if (h >= len) { h = len; break; }
-                if (ldg(seg + h) >= x) break;
+                if (rd(h) >= x) break;
                 l = h + 1;
                 step <<= 1;
             }
             while (l < h) {
                 const uint32_t mid = (l + h) >> 1;
-                if (ldg(seg + mid) < x) l = mid + 1;
+                if (rd(mid) < x) l = mid + 1;
                 else h = mid;
             }
             c = l;
-            v = c < len ? ldg(seg + c) : (K)0;
+            v = c < len ? rd(c) : (K)0;
         }
     }
     *hit = c < len && v == x;
@@ -174,7 +176,8 @@ k_seg_sorted(const SegParams<K> p) {
     constexpr uint32_t S = 1u << D;
     extern __shared__ __align__(16) uint32_t sm[];
     uint32_t* F = sm;                                         // slot 0: segment max; 1..S-1: Eytzinger
-    uint64_t* bnd = reinterpret_cast<uint64_t*>(sm + S);      // query ranges of this CTA's segments
+    K* SK = reinterpret_cast<K*>(sm + S);                     // [S] the segment's keys (the candidate reads)
+    uint64_t* bnd = reinterpret_cast<uint64_t*>(SK + S);      // query ranges of this CTA's segments
     const uint64_t G = gridDim.x, B = p.B, n = p.n, m = p.m;
     const uint64_t b0 = B * blockIdx.x / G, b1 = B * (blockIdx.x + 1) / G;
     const uint32_t nb = (uint32_t)(b1 - b0);
@@ -215,6 +218,7 @@ k_seg_sorted(const SegParams<K> p) {
             const uint32_t i = k * 1024u + threadIdx.x;
             const uint32_t f = i < len ? seg_image(kk[k], smin, sh) : 0xFFFFFFFFu;
             F[i == S - 1 ? 0u : eytz_slot<D>(i)] = f;
+            SK[i] = kk[k];
         }
         __syncthreads();
         const K lower = b ? ldg(p.a + lo - 1) : (K)0;
@@ -250,7 +254,7 @@ k_seg_sorted(const SegParams<K> p) {
                 uint64_t lb;
                 bool hit;
                 if ((first || x[r] > lower) && (last || x[r] <= smax)) {
-                    lb = lo + seg_finish<K, D>(F, seg, len, smin, sh, x[r], kq[r], &hit);
+                    lb = lo + seg_finish<K, D, true>(F, SK, len, smin, sh, x[r], kq[r], &hit);
                 } else {
                     // outside the segment's key range (an unsorted batch): plain bisection
                     lb = lower_bound_global(p.a, n, x[r]);
@@ -694,11 +698,11 @@ k_unpart(const PartParams<K> p) {
 
 // ---------------------------------------------------------------- launchers
 
-static uint64_t seg_smem_bytes(uint64_t n, uint32_t grid) {
+static uint64_t seg_smem_bytes(uint64_t n, uint32_t grid, uint32_t kb) {
     const uint64_t S = 1ull << kSegLog2;
     const uint64_t B = (n + S - 1) / S;
     const uint64_t nb = (B + grid - 1) / grid + 1;
-    return S * 4 + nb * 8 + 16;
+    return S * (4 + kb) + nb * 8 + 16;
 }
 
 template <class K, int D, int OB>
@@ -708,7 +712,7 @@ static cudaError_t go_seg(const SegParams<K>& p, Grid grid, cudaStream_t s, bool
     uint64_t g = 0;
     grid.sched_static = 1;
     grid.ctas_per_sm = 1;
-    const uint32_t smem = (uint32_t)seg_smem_bytes(p.n, grid.sm_count);
+    const uint32_t smem = (uint32_t)seg_smem_bytes(p.n, grid.sm_count, (uint32_t)sizeof(K));
     cudaError_t e = plan_grid((const void*)kern, threads, smem, grid, grid.sm_count, carveout_for(smem, threads), &g, uns);
     if (e != cudaSuccess || *uns) return e;
     kern<<<(unsigned)g, threads, smem, s>>>(p);
@@ -720,7 +724,7 @@ cudaError_t launch_seg_sorted(int kb, int ob, const void* a, uint64_t n, const v
                               uint32_t stream_hint, Grid grid, cudaStream_t s, bool* uns) {
     constexpr int D = kSegLog2;
     const uint64_t S = 1ull << D;
-    if (seg_smem_bytes(n, grid.sm_count) > 200u * 1024u) { *uns = true; return cudaSuccess; }
+    if (seg_smem_bytes(n, grid.sm_count, (uint32_t)kb) > 200u * 1024u) { *uns = true; return cudaSuccess; }
     if (kb == 8) {
         SegParams<uint64_t> p{(const uint64_t*)a, n, (const uint64_t*)q, m, out, (uint32_t)ob, (n + S - 1) / S, stream_hint};
         return ob == 8 ? go_seg<uint64_t, D, 8>(p, grid, s, uns) : go_seg<uint64_t, D, 4>(p, grid, s, uns);
