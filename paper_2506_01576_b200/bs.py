@@ -18,7 +18,8 @@ import re
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libbs.so")
+# BS_LIB_PATH: another build of the same library (A/B timing runs in tools/)
+LIB_PATH = os.environ.get("BS_LIB_PATH") or os.path.join(_HERE, "lib", "libbs.so")
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "bs.h")
 
 BS_OK, BS_ERR_INVALID, BS_ERR_UNSUPPORTED, BS_ERR_OOM, BS_ERR_CUDA, BS_ERR_NCCL, BS_ERR_NOT_SORTED = 0, -1, -2, -3, -4, -5, -6

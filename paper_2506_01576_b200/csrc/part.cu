@@ -305,12 +305,30 @@ __device__ __forceinline__ uint32_t bk_exscan(uint32_t* v, uint32_t N, uint32_t*
     return total;
 }
 
+// two consecutive keys with one vector load (16 B for u64, 8 B for u32), streaming
+template <class K>
+__device__ __forceinline__ void ld_pair(const K* p, uint64_t pol, K& x0, K& x1) {
+    if constexpr (sizeof(K) == 8) {
+        uint64_t a, b;
+        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u64 {%0,%1}, [%2], %3;"
+                     : "=l"(a), "=l"(b) : "l"(p), "l"(pol));
+        x0 = a; x1 = b;
+    } else {
+        uint32_t a, b;
+        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;"
+                     : "=r"(a), "=r"(b) : "l"(p), "l"(pol));
+        x0 = a; x1 = b;
+    }
+}
+
 // ---- pass 1: per-CTA histograms (same tile -> CTA map as k_bk_part); the next
-// tile's queries are in flight while this tile is bucketed
+// tile's queries are in flight while this tile is bucketed.  Each thread takes
+// pairs of neighbouring queries (one vector load, one 4-B store of the two
+// bucket ids): the pass is issue-bound, not bandwidth-bound.
 template <class K>
 __global__ void __launch_bounds__(kBkPThreads, kBkPCtas)
 k_bk_hist(const BkParams<K> p) {
-    constexpr uint32_t T = kBkTile, E = T / kBkPThreads;
+    constexpr uint32_t T = kBkTile, E2 = T / kBkPThreads / 2;   // pairs per thread per tile
     extern __shared__ __align__(16) uint32_t sm[];
     const uint32_t B4 = (p.B + 3u) & ~3u;
     uint32_t* MS = sm;
@@ -323,34 +341,47 @@ k_bk_hist(const BkParams<K> p) {
     const uint64_t ntiles = (p.m + T - 1) / T;
     auto load_tile = [&](uint64_t t, K* xs) {
         const uint64_t b0 = t * T;
+        const bool full = t < ntiles && b0 + T <= p.m;
 #pragma unroll
-        for (uint32_t e = 0; e < E; ++e) {
-            const uint64_t j = b0 + e * kBkPThreads + threadIdx.x;
-            xs[e] = (t < ntiles && j < p.m) ? load_stream(p.q + j, true, pol) : (K)0;
+        for (uint32_t e = 0; e < E2; ++e) {
+            const uint64_t j = b0 + 2 * (e * kBkPThreads + threadIdx.x);
+            if (full) {
+                ld_pair<K>(p.q + j, pol, xs[2 * e], xs[2 * e + 1]);
+            } else {
+                xs[2 * e] = (t < ntiles && j < p.m) ? load_stream(p.q + j, true, pol) : (K)0;
+                xs[2 * e + 1] = (t < ntiles && j + 1 < p.m) ? load_stream(p.q + j + 1, true, pol) : (K)0;
+            }
         }
     };
-    constexpr bool PF = E <= 8;   // the next tile in flight when the registers allow it
-    K xn[PF ? E : 1];
+    constexpr bool PF = E2 <= 4;   // the next tile in flight when the registers allow it
+    K xn[PF ? 2 * E2 : 1];
     if constexpr (PF) load_tile(blockIdx.x, xn);
     for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const uint64_t b0 = t * T;
         const uint32_t cntq = (uint32_t)((p.m - b0) < T ? (p.m - b0) : T);
-        K x[E];
+        K x[2 * E2];
         if constexpr (PF) {
 #pragma unroll
-            for (uint32_t e = 0; e < E; ++e) x[e] = xn[e];
+            for (uint32_t e = 0; e < 2 * E2; ++e) x[e] = xn[e];
             load_tile(t + gridDim.x, xn);
         } else {
             load_tile(t, x);
         }
 #pragma unroll
-        for (uint32_t e = 0; e < E; ++e) {
-            const uint32_t j = e * kBkPThreads + threadIdx.x;
-            if (j < cntq) {
-                const uint32_t b = bk_bucket(p, MS, DIR, x[e]);
-                atomicAdd(&hist[b], 1u);
-                __stcs(p.bkid + b0 + j, (uint16_t)b);   // the partition pass reads it back
+        for (uint32_t e = 0; e < E2; ++e) {
+            const uint32_t j = 2 * (e * kBkPThreads + threadIdx.x);
+            uint32_t b01 = 0;
+#pragma unroll
+            for (uint32_t h = 0; h < 2; ++h) {
+                if (j + h < cntq) {
+                    const uint32_t b = bk_bucket(p, MS, DIR, x[2 * e + h]);
+                    atomicAdd(&hist[b], 1u);
+                    b01 |= b << (16 * h);
+                }
             }
+            // the partition pass reads the bucket ids back
+            if (j + 1 < cntq) __stcs(reinterpret_cast<uint32_t*>(p.bkid + b0 + j), b01);
+            else if (j < cntq) __stcs(p.bkid + b0 + j, (uint16_t)b01);
         }
     }
     __syncthreads();
