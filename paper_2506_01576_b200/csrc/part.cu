@@ -931,7 +931,14 @@ cudaError_t launch_bucket(int kb, int ob, const BucketIndex& bi, const void* a, 
         p.B = (uint32_t)bi.B; p.D = bi.D; p.NB = bi.NB; p.LB = bi.LB;
         p.tab = bi.tab; p.par = bi.par; p.mx = bi.mx; p.dir = bi.dir; p.gnode = bi.gnode;
         p.gbase = bi.gbase; p.gsh = bi.gsh;
-        p.CH = chunk ? chunk : kBkChunk;
+        // search items: a window of ~37 buckets' queries across the CTAs (L2-sized),
+        // at most kBkChunk (the config-3 optimum) and at least 4096 queries
+        uint64_t ch = chunk;
+        if (!ch) {
+            ch = m * 37 / ((uint64_t)sm_count * bi.B);
+            ch = ch > kBkChunk ? kBkChunk : (ch < 4096 ? 4096 : ch);
+        }
+        p.CH = (uint32_t)ch;
     };
     if (kb == 8) {
         BkParams<uint64_t> p{};
