@@ -110,3 +110,16 @@ def test_parity_partitioned_gloo_world2():
                           np.array([0, (1 << 64) - 1, 1 << 40], dtype=np.uint64)]) for _ in range(2)]
     want = [oracle.lookup(keys, q, out_bytes=8) for q in qs]
     mp.spawn(_parity_worker, args=(2, _free_port(), keys, cuts, qs, want, 17), nprocs=2, join=True)
+
+
+def test_default_reorder_per_config():
+    """bench.py times the config's fastest mode by default: the
+    key-range partition for random batches over arrays larger than L2, the
+    segment-staged lookup for pre-sorted batches, the plain kernels otherwise."""
+    import bench
+    assert bench.default_reorder("config3", "random") == 5
+    assert bench.default_reorder("config4", "random") == 5
+    assert bench.default_reorder("config3", "sorted") == 3
+    assert bench.default_reorder("config2", "random") == 0
+    assert bench.default_reorder("config1", "random") == 0
+    assert bench.default_reorder("config5", "random") == 0
