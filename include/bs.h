@@ -75,14 +75,14 @@ typedef enum {
                               coarse) into buckets whose slice of the array stays L2-resident
                               while it is searched: a histogram pass, a partition pass
                               (bucket-major regions, exact offsets), the per-bucket search, one
-                              pass restoring query order.  Fine buckets (n <= 2^27 u64 / 2^28
-                              u32 keys): 2^15 leaves of 32 B, searched through the bucket's
-                              pinned Eytzinger table of leaf maxima staged in shared memory by
-                              TMA (§4.2) and one 32-B leaf (§5).  Coarse buckets (larger n, up
-                              to 2^31 u64 / 2^32 u32 keys): 16-MB key slices searched by the
-                              index's own kernel over the partitioned batch.  Any variant's
-                              index (bs_build always builds the bucket tables: n * key / 8
-                              bytes when fine).  Needs bs_lookup_ws.                         */
+                              pass restoring query order.  Per bucket bs_build builds a pinned
+                              Eytzinger table (§4.2) staged into shared memory by TMA.  Fine
+                              buckets (n <= 2^27 u64 / 2^28 u32 keys): the table holds the
+                              maxima of 2^15 leaves of 32 B, then one leaf is read (§5).
+                              Two-level buckets (larger n, up to 2^31 u64 / 2^32 u32 keys):
+                              16 MB of keys; the table holds the maxima of 2^15 units of 8
+                              leaves of 64 B, a 32-B node per unit the 8 leaf maxima.  Any
+                              variant's index.  Needs bs_lookup_ws.                          */
 } bs_reorder;
 
 /* Build-time structure + default launch configuration.

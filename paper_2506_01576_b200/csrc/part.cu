@@ -10,27 +10,31 @@
 // after bucket, and restores query order — a coarse global reorder that costs
 // three streaming passes instead of a sort:
 //
-//   k_bk_hist    per CTA: histogram of its tiles' queries over the B buckets
+//   k_bk_hist    per CTA: histogram of its tiles' queries over the B buckets;
+//                each query's bucket id is stored for the partition pass
 //   k_bk_scan    per bucket: exclusive prefix of the CTA histograms
-//   k_bk_part    per tile of T queries: bucket each query, counting-sort the tile
-//                by bucket in shared memory, append each bucket's run to the
-//                CTA's slice of that bucket's region (bucket-major, exact
-//                offsets: no atomics in global memory, no overflow), and record
-//                for every sorted position its bucket and original slot
-//   k_bk_search  items of CH queries in bucket order: per bucket, a pinned
-//                Eytzinger table of its 2^D leaf maxima (§4.2's pinned top
-//                levels of a binary search, built by bs_build) is staged once by
-//                TMA; each lookup descends D levels in shared memory, reads its
-//                32-B leaf (one sector, L2-resident while the bucket is worked
-//                on) and counts the keys < q (§5's leaf scan)
+//   k_bk_part    per tile of T = 8192 queries: rank each query in its bucket's
+//                run (shared atomic), counting-sort the tile by bucket in shared
+//                memory, append each run to the CTA's slice of its bucket's
+//                region (bucket-major, exact offsets: no global atomics, no
+//                overflow), and record for every sorted position its bucket and
+//                original slot
+//   k_bk_search  items of queries in bucket order from a global counter: per
+//                bucket a pinned Eytzinger table of its 2^D unit maxima (§4.2's
+//                pinned top levels of a binary search, built by bs_build) is
+//                staged by TMA; each lookup descends D levels in shared memory,
+//                then (two-level buckets) reads one 32-B node of leaf-maxima
+//                images, then reads its leaf (L2-resident while the bucket is
+//                worked on) and counts the keys < q (§5's leaf scan)
 //   k_bk_unpart  per tile: gather the results of its runs, scatter them to query
 //                order in shared memory, one coalesced store (Listing 2 l.35-39's
 //                "unsort", at batch scale)
 //
-// Bucket b covers the array positions [b*NB, (b+1)*NB), NB = 2^D leaves of LK
-// keys (LK = 32 B / key); a query belongs to bucket #(bucket maxima < q) (the
-// last bucket also takes the queries above every key).  The bucket is exact, so
-// the per-bucket search never leaves its bucket.
+// Bucket b covers the array positions [b*NB, (b+1)*NB): fine buckets hold 2^D
+// leaves of 32 B (NB = 2^17 u64 / 2^18 u32 keys), two-level buckets 2^D units of
+// 8 leaves of 64 B (16 MB of keys).  A query belongs to bucket #(bucket maxima <
+// q) (the last bucket also takes the queries above every key).  The bucket is
+// exact, so the per-bucket search never leaves its bucket.  DESIGN.md §6.11.
 #include <cstdlib>
 #include <cstring>
 #include <type_traits>
