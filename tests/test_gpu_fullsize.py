@@ -101,3 +101,26 @@ def test_fullsize_config3_naive_opt(variant):
     idx.close()
     del dk, dq, out
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("cfg", ["config3", "config4"])
+def test_fullsize_bucket(cfg):
+    """BS_REORDER_BUCKET — bench.py's default for configs 3-4 — at full size:
+    fine buckets at config 3 (512 buckets of 2^17 keys), two-level buckets at
+    config 4 (2^30 keys: 512 buckets of 16 MB); sampled oracle + every output's
+    invariant."""
+    n, kb = bench.CONFIGS[cfg][:2]
+    dk, dq, keys, q = _inputs(cfg, "random")
+    m = q.size
+    out = torch.empty(m, dtype=torch.int64, device="cuda")
+    idx = bs.bs_build(dk, n, bs.bs_layout_default(key_bytes=kb, out_bytes=kb))
+    nb = bs.bs_workspace_bytes(idx, m, reorder=bs.REORDER_BUCKET)
+    ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    bs.bs_lookup_ws(idx, dq, m, out, None, ws, nb, reorder=bs.REORDER_BUCKET)
+    torch.cuda.synchronize()
+    samp = np.random.default_rng(13).integers(0, m, size=1 << 16)
+    assert np.array_equal(P.to_numpy_unsigned(out, kb)[samp], oracle.lookup(keys, q[samp], out_bytes=kb))
+    _check_invariant(dk, dq, out, n, kb)
+    idx.close()
+    del dk, dq, out, ws
+    torch.cuda.empty_cache()
