@@ -343,9 +343,11 @@ k_bk_hist(const BkParams<K> p) {
     __syncthreads();
     const uint64_t pol = p.stream_hint ? policy_evict_first() : policy_evict_normal();
     const uint64_t ntiles = (p.m + T - 1) / T;
+    // vector loads need the batch 2-key aligned (bs_lookup only requires key alignment)
+    const bool pairs_ok = ((uintptr_t)p.q & (2 * sizeof(K) - 1)) == 0;
     auto load_tile = [&](uint64_t t, K* xs) {
         const uint64_t b0 = t * T;
-        const bool full = t < ntiles && b0 + T <= p.m;
+        const bool full = pairs_ok && t < ntiles && b0 + T <= p.m;
 #pragma unroll
         for (uint32_t e = 0; e < E2; ++e) {
             const uint64_t j = b0 + 2 * (e * kBkPThreads + threadIdx.x);
@@ -809,7 +811,7 @@ k_bk_unpart(const BkParams<K> p) {
         }
         __syncthreads();
         O* out = (O*)p.out + b0;
-        if (cntq == T && OB == 8) {
+        if (cntq == T && OB == 8 && ((uintptr_t)p.out & 15) == 0) {
             // 16-B stores: two results per thread per step
             for (uint32_t j = threadIdx.x * 2; j < T; j += blockDim.x * 2) {
                 const uint2 lo = *reinterpret_cast<const uint2*>(so + j);

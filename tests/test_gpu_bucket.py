@@ -195,3 +195,25 @@ def test_bucket_two_level_distributions(kind, monkeypatch):
         idx = build(keys, variant=bs.KARY, out_bytes=8)
         check(bk_run(idx, q, 8), want, q, f"two-level {kind} lb32={lb32}")
         idx.close()
+
+
+@pytest.mark.parametrize("kb", [4, 8])
+def test_bucket_unaligned_buffers(kb):
+    """Queries and results only key- / word-aligned (not 16-B aligned): the vector
+    loads of the histogram pass and the vector stores of the unpartition pass
+    fall back to scalar accesses."""
+    keys = workload.gen_keys(3 * NB[kb] + 5, kb, seed=51)
+    q = queries_for(keys, 5 * T + 3, 52, "random")
+    want = oracle.lookup(keys, q, out_bytes=8)
+    idx = build(keys, variant=bs.KARY, out_bytes=8)
+    big = torch.zeros(q.size + 4, dtype={4: torch.int32, 8: torch.int64}[kb], device="cuda")
+    dq = big[1:1 + q.size]                      # 4 / 8 B past a 16-B boundary
+    dq.copy_(P.as_torch(q))
+    obig = torch.full((q.size + 2,), -1, dtype=torch.int64, device="cuda")
+    out = obig[1:1 + q.size]                    # 8 B past a 16-B boundary
+    nb = bs.bs_workspace_bytes(idx, q.size, reorder=bs.REORDER_BUCKET)
+    ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    bs.bs_lookup_ws(idx, dq, q.size, out, None, ws, nb, reorder=bs.REORDER_BUCKET)
+    torch.cuda.synchronize()
+    check(P.to_numpy_unsigned(out, 8), want, q, f"unaligned kb={kb}")
+    idx.close()
