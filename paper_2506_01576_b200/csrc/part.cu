@@ -429,7 +429,7 @@ k_bk_scan(uint32_t* __restrict__ cnt, uint32_t* __restrict__ tot, uint32_t G, ui
 
 // ---- pass 3: partition (tile t on CTA t % G, as in k_bk_hist)
 //
-// Thread i owns buckets [i BPT, (i+1) BPT) (BPT = ceil(B / threads) <= 2): their
+// Thread i owns buckets [i BPT, (i+1) BPT) (BPT = kBkFineMax / threads = 1): their
 // tile counts, run starts and global cursors live in its registers, so a tile
 // costs four barriers (ranks / warp totals / run starts / sorted tile) and no
 // loops over the buckets; the next tile's queries and bucket ids are in flight
