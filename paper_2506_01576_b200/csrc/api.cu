@@ -387,8 +387,8 @@ const char* bs_version(void) {
 // BS_REORDER_BUCKET structures (part.cu).  Fine: buckets of 2^D units of one
 // 32-B leaf (D = 15; BS_BUCKET_D = 14 for A/B runs) while that needs <=
 // kBkFineMax buckets (n <= 2^27 u64 / 2^28 u32 keys); above, two-level buckets:
-// 2^15 units of 8 leaves of 64 B (16 MB of keys per bucket) with one 32-B node of
-// leaf-maxima images per unit, up to kBkMaxBuckets (n <= 2^31 u64 / 2^32 u32).
+// 2^15 units of 16 leaves of 32 B (16 MB of keys per bucket) with one 32-B node of
+// 16-bit leaf-maxima images per unit, up to kBkMaxBuckets (n <= 2^31 u64 / 2^32 u32).
 // Tables, per-bucket image parameters, nodes, bucket maxima and their directory
 // in one allocation.  Not built (the mode reports UNSUPPORTED) above that.
 static int build_bucket_layout(Index* ix, cudaStream_t st, BuildTimer& bt) {
@@ -399,13 +399,15 @@ static int build_bucket_layout(Index* ix, cudaStream_t st, BuildTimer& bt) {
     uint64_t B = (ix->n + NB - 1) / NB;
     uint32_t LB = 32;
     if (B > kBkFineMax || force_two) {
-        // 64-B leaves (16-MB buckets).  Measured at config 4: 32-B leaves (8-MB
-        // buckets, 1024 of them; BS_BUCKET_LB32=1) ran the search at 25.5 vs 23.0
-        // ms and moved 67 vs 26 DRAM B / lookup
+        // units of 16 leaves of 32 B with a node of 16-bit images relative to the
+        // unit (16-MB buckets): per lookup one node sector and one leaf sector.
+        // A/B knob BS_BUCKET_G8=1: units of 8 leaves of 64 B with 32-bit node images
+        // (the previous layout: one node sector and two leaf sectors)
         D = 15;
-        G = 8;
-        LB = (getenv("BS_BUCKET_LB32") && atoi(getenv("BS_BUCKET_LB32")) != 0) ? 32u : 64u;
-        NB = (8ull << D) * (LB / ix->kb);
+        const bool g8 = getenv("BS_BUCKET_G8") && atoi(getenv("BS_BUCKET_G8")) != 0;
+        G = g8 ? 8u : 16u;
+        LB = g8 ? 64u : 32u;
+        NB = ((uint64_t)G << D) * (LB / ix->kb);
         B = (ix->n + NB - 1) / NB;
     }
     if (B > kBkMaxBuckets) return BS_OK;
@@ -413,7 +415,8 @@ static int build_bucket_layout(Index* ix, cudaStream_t st, BuildTimer& bt) {
     if (e != cudaSuccess) return fail_cuda(e, "bucket tables: sync");
     auto al = [](uint64_t x) { return (x + 255) & ~255ull; };
     const uint64_t o_tab = 0, o_par = al(4 * (B << D)), o_gn = o_par + al(16 * B);
-    const uint64_t o_mx = o_gn + (G > 1 ? al(4 * (B << D) * G) : 0), o_dir = o_mx + al(4 * B);
+    const uint64_t gn_bytes = G == 16 ? 2 * (B << D) * G : G > 1 ? 4 * (B << D) * G : 0;
+    const uint64_t o_mx = o_gn + al(gn_bytes), o_dir = o_mx + al(4 * B);
     const uint64_t total = o_dir + al(2 * ((1u << 13) + 1));
     e = cudaMalloc(&ix->d_bk, total);
     if (e != cudaSuccess) return fail_cuda(e, "cudaMalloc(bucket tables)");

@@ -120,8 +120,8 @@ cudaError_t launch_part_global(int kb, int ob, const void* a, uint64_t n, const 
 // slice of the array stays L2-resident while it is searched.  Each bucket has a
 // pinned Eytzinger table of 2^D unit maxima images (built by bs_build, staged by
 // TMA).  Fine buckets (n <= 2^27 u64 / 2^28 u32 keys): a unit is one 32-B leaf.
-// Two-level buckets (larger n): a unit is 8 leaves of 64 B (16-MB slices), with a
-// 32-B global node of the 8 leaf maxima images per unit.
+// Two-level buckets (larger n): a unit is 16 leaves of 32 B (16-MB slices), with a
+// 32-B global node of the 16 leaf maxima images (16-bit, relative to the unit).
 constexpr uint32_t kBkFineMax = 1024;       // most buckets (the partition pass keeps two buckets'
 constexpr uint32_t kBkMaxBuckets = 1024;    // state per thread in registers; runs stay long)
 constexpr uint32_t kBkChunk = 65536;        // queries per search item (measured at config 3: 8192 3.29 ms,
@@ -130,11 +130,12 @@ struct BucketIndex {
     uint64_t B = 0;              // buckets
     uint64_t NB = 0;             // keys per bucket (power of two); bucket b = positions [b NB, (b+1) NB)
     uint32_t D = 0;              // table depth: 2^D units per bucket
-    uint32_t G = 1;              // leaves per unit: 1 (fine) or 8 (two-level)
-    uint32_t LB = 32;            // leaf bytes: 32 (fine), 64 (two-level)
+    uint32_t G = 1;              // leaves per unit: 1 (fine), 16 (two-level; 8 with BS_BUCKET_G8=1)
+    uint32_t LB = 32;            // leaf bytes: 32 (64 with BS_BUCKET_G8=1)
     const uint32_t* tab = nullptr;   // [B << D] unit-maxima images, Eytzinger order per bucket
     const uint64_t* par = nullptr;   // [2B] per-bucket image base, shift
-    const uint32_t* gnode = nullptr; // G = 8: [(B << D) * 8] leaf-maxima images in leaf order
+    const uint32_t* gnode = nullptr; // two-level: per unit one 32-B node of leaf-maxima images (G = 16:
+                                     // 16-bit, relative to the unit; G = 8: 32-bit)
     const uint32_t* mx = nullptr;    // [B] bucket-maxima images under the global image
     const uint16_t* dir = nullptr;   // [2^13 + 1] radix directory over mx
     uint64_t gbase = 0;          // global image: min((x - gbase) >> gsh, 2^32 - 1), 0 below gbase

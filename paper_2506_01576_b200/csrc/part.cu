@@ -154,6 +154,48 @@ __global__ void k_bk_build_gnode(const K* __restrict__ a, uint64_t n, uint32_t D
     gnode[g] = f;
 }
 
+// Two-level buckets with 16-leaf units (G = 16): per unit one 32-B node of 16
+// 16-bit images of its leaf maxima, RELATIVE to the unit's image range: with
+// lo = image of unit u-1's maximum (0 for u = 0) and hi = image of unit u's
+// maximum (2^32 - 1 for the last unit, which the table does not hold), s =
+// bitlen(hi - lo) - 16 (>= 0), g = min((image - lo) >> s, 2^16 - 1).  The
+// search's descent sees exactly these lo / hi (the last probes below and at or
+// above q's image), so the query's g uses the same s.  Leaves past the array:
+// 0xFFFF.  Uses the bucket parameters written by k_bk_build_tab.
+__device__ __forceinline__ uint32_t bk_sub_shift(uint32_t lo, uint32_t hi) {
+    const uint32_t span = hi - lo;
+    const uint32_t bl = span ? 32u - (uint32_t)__clz((int)span) : 0u;
+    return bl > 16u ? bl - 16u : 0u;
+}
+
+template <class K>
+__global__ void k_bk_build_gnode16(const K* __restrict__ a, uint64_t n, uint32_t D, uint32_t LK, uint64_t B,
+                                   const uint64_t* __restrict__ par, uint16_t* __restrict__ gnode) {
+    constexpr uint32_t G = 16;
+    const uint64_t per = (uint64_t)G << D, NB = per * LK, S = 1ull << D;
+    const uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= B * per) return;
+    const uint64_t b = g / per, i = g % per, u = i / G;
+    const uint64_t lo = b * NB, len = (n - lo) < NB ? (n - lo) : NB;
+    const uint64_t base = par[2 * b];
+    const uint32_t sh = (uint32_t)par[2 * b + 1];
+    auto unit_max_img = [&](uint64_t v) -> uint32_t {   // image of unit v's maximum (0xFFFFFFFF past the keys)
+        if (v * G * LK >= len) return 0xFFFFFFFFu;
+        const uint64_t e = (v + 1) * G * LK < len ? (v + 1) * G * LK : len;
+        return bk_img((uint64_t)a[lo + e - 1], base, sh);
+    };
+    const uint32_t flo = u == 0 ? 0u : unit_max_img(u - 1);
+    const uint32_t fhi = u + 1 == S ? 0xFFFFFFFFu : unit_max_img(u);
+    uint16_t r = 0xFFFFu;
+    if (i * LK < len) {
+        const uint64_t e = (i + 1) * LK < len ? (i + 1) * LK : len;
+        const uint32_t f = bk_img((uint64_t)a[lo + e - 1], base, sh);
+        const uint32_t d = (f > flo ? f - flo : 0u) >> bk_sub_shift(flo, fhi);
+        r = (uint16_t)(d > 0xFFFFu ? 0xFFFFu : d);
+    }
+    gnode[g] = r;
+}
+
 cudaError_t build_bucket_index(int kb, const void* a, uint64_t n, uint32_t D, uint32_t G, uint32_t LB, uint64_t NB,
                                uint64_t B, uint64_t gbase, uint32_t gsh, uint32_t* tab, uint64_t* par, uint32_t* gnode,
                                uint32_t* mx, uint16_t* dir, cudaStream_t s) {
@@ -168,7 +210,10 @@ cudaError_t build_bucket_index(int kb, const void* a, uint64_t n, uint32_t D, ui
         if (G > 1) {
             const uint64_t tn = (B << D) * G;
             const uint32_t g3 = (uint32_t)((tn + 255) / 256);
-            if (kb == 8) k_bk_build_gnode<uint64_t><<<g3, 256, 0, s>>>((const uint64_t*)a, n, D, LK, G, B, par, gnode);
+            uint16_t* g16 = reinterpret_cast<uint16_t*>(gnode);
+            if (G == 16 && kb == 8) k_bk_build_gnode16<uint64_t><<<g3, 256, 0, s>>>((const uint64_t*)a, n, D, LK, B, par, g16);
+            else if (G == 16) k_bk_build_gnode16<uint32_t><<<g3, 256, 0, s>>>((const uint32_t*)a, n, D, LK, B, par, g16);
+            else if (kb == 8) k_bk_build_gnode<uint64_t><<<g3, 256, 0, s>>>((const uint64_t*)a, n, D, LK, G, B, par, gnode);
             else k_bk_build_gnode<uint32_t><<<g3, 256, 0, s>>>((const uint32_t*)a, n, D, LK, G, B, par, gnode);
         }
     }
@@ -189,15 +234,16 @@ struct BkParams {
     uint32_t B;              // buckets
     uint32_t D;              // per-bucket table depth: 2^D units per bucket
     uint32_t LB;             // leaf bytes (32 or 64)
+    uint32_t G;              // leaves per unit (1, 8 or 16)
     uint64_t NB;             // keys per bucket = 2^D * LK
     const uint32_t* tab;     // [B << D] per-bucket Eytzinger tables of unit maxima images
-    const uint32_t* gnode;   // two-level: [(B << D) * 8] leaf maxima images, 8 per unit
+    const uint32_t* gnode;   // two-level: one 32-B node of leaf-maxima images per unit
     const uint64_t* par;     // [2B] per-bucket image base, shift
     const uint32_t* mx;      // [B] global images of the bucket maxima
     const uint16_t* dir;     // [kBkBins + 1] radix directory over mx
     uint64_t gbase;          // global image: bk_img(x, gbase, gsh)
     uint32_t gsh;
-    uint32_t G;              // CTAs of hist / part / unpart (tile t on CTA t % G)
+    uint32_t Gp;             // CTAs of hist / part / unpart (tile t on CTA t % Gp)
     uint32_t Gs;             // CTAs of the search (one per SM)
     uint32_t CH;             // queries per search item
     uint32_t stream_hint;
@@ -653,12 +699,17 @@ __device__ __forceinline__ void bk_finish(const K* __restrict__ ab, uint64_t klo
 // batch k+1 descends) ran 3 % slower — the kernel is bound by the L1 data pipe
 // (shared-memory bank conflicts of the random probes + one leaf wavefront per
 // lookup), not by latency.
+// threads of the search: 768 for 16-leaf units (80 registers: the node and the
+// leaf of two lookups in flight), else 1024
+constexpr uint32_t bk_search_threads(int G) { return G == 16 ? 768u : kBkThreads; }
+
 template <class K, int OB, int D, int G, int LV>
-__global__ void __launch_bounds__(kBkThreads, 1)
+__global__ void __launch_bounds__(bk_search_threads(G), 1)
 k_bk_search(const BkParams<K> p) {
     // LV: leaf size in u64 words (4: 32 B, 8: 64 B)
     constexpr uint32_t LK = 8u * LV / sizeof(K);            // keys per leaf
-    constexpr uint32_t R = LV == 4 ? 4 : 2;                 // lookups in flight per thread
+    constexpr uint32_t R = (G == 1 && LV == 4) ? 4 : 2;    // lookups in flight per thread
+    constexpr uint32_t TS = bk_search_threads(G);
     constexpr uint32_t S = 1u << D;
     extern __shared__ __align__(16) uint32_t sm[];
     const uint32_t B = p.B;
@@ -713,29 +764,55 @@ k_bk_search(const BkParams<K> p) {
         const uint64_t len = (p.n - klo) < p.NB ? (p.n - klo) : p.NB;
         const uint32_t Mb = (uint32_t)((len + LK - 1) / LK);   // leaves holding keys
         const K* ab = p.a + klo;
-        const uint32_t* gn = p.gnode + ((uint64_t)b << D) * G;  // G = 8: leaf maxima images, 8 per unit
-        for (uint32_t i = i0 + threadIdx.x; i < i1; i += kBkThreads * R) {
+        // G = 8: u32 leaf-maxima images, 8 per unit; G = 16: u16 images relative to the unit
+        const uint32_t* gn = p.gnode + ((uint64_t)b << D) * (G == 16 ? G / 2 : G);
+        for (uint32_t i = i0 + threadIdx.x; i < i1; i += TS * R) {
             K x[R];
             uint32_t ad[R], fq[R];
+            uint32_t flo[G == 16 ? R : 1], fhi[G == 16 ? R : 1];   // the unit's image range (G = 16)
 #pragma unroll
             for (uint32_t r = 0; r < R; ++r) {
-                const uint32_t ir = i + r * kBkThreads;
+                const uint32_t ir = i + r * TS;
                 x[r] = ir < i1 ? load_stream(p.rq + ir, true, pol_stream) : (K)base;
                 fq[r] = bk_img((uint64_t)x[r], base, sh);
                 ad[r] = sb + 4u;
+                if constexpr (G == 16) { flo[r] = 0u; fhi[r] = 0xFFFFFFFFu; }
             }
 #pragma unroll
             for (uint32_t d = 0; d < (uint32_t)D; ++d) {
 #pragma unroll
                 for (uint32_t r = 0; r < R; ++r) {
                     const uint32_t h = lds_u32(ad[r]);
-                    ad[r] = 2u * ad[r] + (h < fq[r] ? step_lt : step_ge);
+                    const bool lt = h < fq[r];
+                    ad[r] = 2u * ad[r] + (lt ? step_lt : step_ge);
+                    if constexpr (G == 16) {
+                        flo[r] = lt ? h : flo[r];
+                        fhi[r] = lt ? fhi[r] : h;
+                    }
                 }
             }
             uint32_t c[R];
 #pragma unroll
             for (uint32_t r = 0; r < R; ++r) c[r] = ((ad[r] - sb) >> 2) - S;   // unit
-            if constexpr (G > 1) {
+            if constexpr (G == 16) {
+                // the unit's node of 16 leaf-maxima images relative to [flo, fhi] (32 B, one
+                // sector): leaf = 16 u + #(< q's relative image)
+                uint64_t nd[R][4];
+#pragma unroll
+                for (uint32_t r = 0; r < R; ++r)
+                    if (c[r] * G < Mb) ld_sector(gn + (uint64_t)c[r] * (G / 2), pol_leaf, nd[r]);
+#pragma unroll
+                for (uint32_t r = 0; r < R; ++r) {
+                    const uint32_t q16 = (fq[r] - flo[r]) >> bk_sub_shift(flo[r], fhi[r]);   // fq > flo
+                    uint32_t j = 0;
+#pragma unroll
+                    for (uint32_t k = 0; k < 16; ++k) {
+                        const uint32_t im = (uint32_t)(nd[r][k >> 2] >> (16 * (k & 3))) & 0xFFFFu;
+                        j += im < q16 ? 1u : 0u;
+                    }
+                    c[r] = c[r] * G < Mb ? c[r] * G + j : Mb;
+                }
+            } else if constexpr (G > 1) {
                 // the unit's node of G leaf maxima images (32 B, one sector): leaf = G u + #(< q)
                 uint64_t nd[R][4];
 #pragma unroll
@@ -762,7 +839,7 @@ k_bk_search(const BkParams<K> p) {
             }
 #pragma unroll
             for (uint32_t r = 0; r < R; ++r) {
-                const uint32_t ir = i + r * kBkThreads;
+                const uint32_t ir = i + r * TS;
                 if (ir < i1) bk_finish<K, OB, LV>(ab, klo, len, Mb, p.n, x[r], c[r], lv[r], p.rp, ir, pol_leaf, pol_stream);
             }
         }
@@ -876,7 +953,7 @@ static cudaError_t bk_launch(const void* kern, uint32_t threads, uint32_t smem, 
 
 template <class K, int OB>
 static cudaError_t go_bucket(BkParams<K> p, const BkLayout& L, char* ws, cudaStream_t s, int phase, BucketRun* run) {
-    p.G = (uint32_t)L.G;
+    p.Gp = (uint32_t)L.G;
     p.Gs = (uint32_t)L.Gs;
     p.cnt = (uint32_t*)(ws + L.o_cnt);
     p.tot = (uint32_t*)(ws + L.o_tot);
@@ -892,28 +969,29 @@ static cudaError_t go_bucket(BkParams<K> p, const BkLayout& L, char* ws, cudaStr
     if (phase != 2) {
         {
             const uint32_t smem = 8u * B4 + 4u * kBkBins;
-            e = bk_launch((const void*)k_bk_hist<K>, kBkPThreads, smem, p.G, &p, s);
+            e = bk_launch((const void*)k_bk_hist<K>, kBkPThreads, smem, p.Gp, &p, s);
             if (e != cudaSuccess) return e;
         }
-        k_bk_scan<<<(B + 31) / 32, 1024, 0, s>>>(p.cnt, p.tot, p.G, B);
+        k_bk_scan<<<(B + 31) / 32, 1024, 0, s>>>(p.cnt, p.tot, p.Gp, B);
         count_launch();
         {
             const uint32_t smem = kBkTile * ((uint32_t)sizeof(K) + 4u) + 4u * (3u * kBkFineMax + 32u);
-            e = bk_launch((const void*)k_bk_part<K>, kBkPThreads, smem, p.G, &p, s);
+            e = bk_launch((const void*)k_bk_part<K>, kBkPThreads, smem, p.Gp, &p, s);
             if (e != cudaSuccess) return e;
         }
     }
     if (phase == 0) {
         const uint32_t smem = (4u << p.D) + 8u * ((B + 4u) & ~3u) + 4u * 64u + 16u;
         const void* kern = nullptr;
-        if (p.gnode && p.D == 15) kern = p.LB == 32 ? (const void*)k_bk_search<K, OB, 15, 8, 4>
+        if (p.gnode && p.D == 15) kern = p.G == 16 ? (const void*)k_bk_search<K, OB, 15, 16, 4>
+                                       : p.LB == 32 ? (const void*)k_bk_search<K, OB, 15, 8, 4>
                                                     : (const void*)k_bk_search<K, OB, 15, 8, 8>;
         else if (!p.gnode) kern = p.D == 15 ? (const void*)k_bk_search<K, OB, 15, 1, 4>
                                 : p.D == 14 ? (const void*)k_bk_search<K, OB, 14, 1, 4> : nullptr;
         if (!kern) return cudaErrorInvalidValue;
         e = cudaMemsetAsync(p.item_ctr, 0, sizeof(uint32_t), s);
         if (e != cudaSuccess) return e;
-        e = bk_launch(kern, kBkThreads, smem, p.Gs, &p, s);
+        e = bk_launch(kern, bk_search_threads(p.gnode ? (int)p.G : 1), smem, p.Gs, &p, s);
         if (e != cudaSuccess) return e;
     }
     if (phase != 1) {
@@ -934,7 +1012,7 @@ cudaError_t launch_bucket(int kb, int ob, const BucketIndex& bi, const void* a, 
     }
     auto fill = [&](auto& p) {
         p.n = n; p.m = m; p.out = out; p.stream_hint = stream_hint;
-        p.B = (uint32_t)bi.B; p.D = bi.D; p.NB = bi.NB; p.LB = bi.LB;
+        p.B = (uint32_t)bi.B; p.D = bi.D; p.NB = bi.NB; p.LB = bi.LB; p.G = bi.G;
         p.tab = bi.tab; p.par = bi.par; p.mx = bi.mx; p.dir = bi.dir; p.gnode = bi.gnode;
         p.gbase = bi.gbase; p.gsh = bi.gsh;
         // search items: a window of ~37 buckets' queries across the CTAs (L2-sized),

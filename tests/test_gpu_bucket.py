@@ -147,8 +147,9 @@ def test_bucket_config3_sample():
 @pytest.mark.parametrize("kb", [4, 8])
 @pytest.mark.parametrize("variant", [bs.KARY, bs.OPT, bs.NAIVE])
 def test_bucket_two_level(kb, variant, monkeypatch):
-    """Two-level buckets (2^15 units of 8 leaves of 64 B, or of 32 B with the A/B
-    knob BS_BUCKET_LB32=1, a 32-B node of leaf-maxima images per unit) — the layout bs_build picks above 2^27 u64 / 2^28 u32 keys;
+    """Two-level buckets (2^15 units of 16 leaves of 32 B with a 32-B node of 16-bit
+    leaf-maxima images relative to the unit; the A/B knob BS_BUCKET_G8=1: units of
+    8 leaves of 64 B with 32-bit node images) — the layout bs_build picks above 2^27 u64 / 2^28 u32 keys;
     forced here with BS_BUCKET_TWO=1 on arrays of a few buckets.  Also the A/B
     path that searches the partitioned batch with the index's own kernel
     (BS_BUCKET_KARY=1)."""
@@ -160,10 +161,10 @@ def test_bucket_two_level(kb, variant, monkeypatch):
         q = queries_for(keys, 150000, 901, order)
         for ob in ((4, 8) if kb == 4 else (8,)):
             want = oracle.lookup(keys, q, out_bytes=ob)
-            for lb32 in ("0", "1"):
-                monkeypatch.setenv("BS_BUCKET_LB32", lb32)
+            for g8 in ("0", "1"):
+                monkeypatch.setenv("BS_BUCKET_G8", g8)
                 idx = build(keys, variant=variant, out_bytes=ob)
-                check(bk_run(idx, q, ob), want, q, f"two-level kb={kb} v={variant} {order} ob={ob} lb32={lb32}")
+                check(bk_run(idx, q, ob), want, q, f"two-level kb={kb} v={variant} {order} ob={ob} g8={g8}")
                 monkeypatch.setenv("BS_BUCKET_KARY", "1")
                 check(bk_run(idx, q, ob), want, q, f"partitioned own-kernel kb={kb} v={variant} {order} ob={ob}")
                 monkeypatch.delenv("BS_BUCKET_KARY")
@@ -190,10 +191,10 @@ def test_bucket_two_level_distributions(kind, monkeypatch):
     keys = np.sort(v)
     q = queries_for(keys, 200000, 34, "random")
     want = oracle.lookup(keys, q, out_bytes=8)
-    for lb32 in ("0", "1"):
-        monkeypatch.setenv("BS_BUCKET_LB32", lb32)
+    for g8 in ("0", "1"):
+        monkeypatch.setenv("BS_BUCKET_G8", g8)
         idx = build(keys, variant=bs.KARY, out_bytes=8)
-        check(bk_run(idx, q, 8), want, q, f"two-level {kind} lb32={lb32}")
+        check(bk_run(idx, q, 8), want, q, f"two-level {kind} g8={g8}")
         idx.close()
 
 
