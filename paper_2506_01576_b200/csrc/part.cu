@@ -1015,11 +1015,13 @@ cudaError_t launch_bucket(int kb, int ob, const BucketIndex& bi, const void* a, 
         p.B = (uint32_t)bi.B; p.D = bi.D; p.NB = bi.NB; p.LB = bi.LB; p.G = bi.G;
         p.tab = bi.tab; p.par = bi.par; p.mx = bi.mx; p.dir = bi.dir; p.gnode = bi.gnode;
         p.gbase = bi.gbase; p.gsh = bi.gsh;
-        // search items: a window of ~37 buckets' queries across the CTAs (L2-sized),
+        // search items: the CTAs' window of items spans ~37 MB of keys (config 3:
+        // 37 fine buckets of 1 MB; config 4: ~2.3 two-level buckets of 16 MB),
         // at most kBkChunk (the config-3 optimum) and at least 4096 queries
         uint64_t ch = chunk;
         if (!ch) {
-            ch = m * 37 / ((uint64_t)sm_count * bi.B);
+            const uint64_t bucket_bytes = bi.NB * (uint64_t)kb;
+            ch = (uint64_t)((double)m * (37.0 * (1 << 20) / (double)bucket_bytes) / ((double)sm_count * (double)bi.B));
             ch = ch > kBkChunk ? kBkChunk : (ch < 4096 ? 4096 : ch);
         }
         p.CH = (uint32_t)ch;
