@@ -89,12 +89,12 @@ def algorithmic_bytes_per_lookup(cfg: str, kb: int, ob: int, order: str, n: int,
 def default_reorder(cfg: str, order: str) -> int:
     """The mode bench.py times by default: the key-range
     partition (BS_REORDER_BUCKET) for a random batch over an array much larger
-    than L2, the segment-staged lookup (BS_REORDER_SORTED) for a sorted batch,
-    the plain K-ary kernel otherwise (L2-resident arrays, the peer path)."""
+    than L2 (for config 5: the bucket pipeline over each rank's receive window,
+    bs_build_peer with layout.reorder = BUCKET), the segment-staged lookup
+    (BS_REORDER_SORTED) for a sorted batch, the plain K-ary kernel otherwise
+    (L2-resident arrays)."""
     n, kb, _, _, mode, _ = CONFIGS[cfg]
-    if mode == "partitioned":
-        return 0
-    if order == "sorted":
+    if order == "sorted" and mode != "partitioned":
         return 3
     return 5 if n * kb > (256 << 20) else 0
 

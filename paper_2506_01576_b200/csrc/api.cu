@@ -113,7 +113,6 @@ cudaError_t plan_grid(const void* kern, uint32_t threads, uint32_t smem, Grid gr
     return cudaSuccess;
 }
 
-static uint64_t bucket_max_keys(uint32_t kb) { return (uint64_t)kBkMaxBuckets * ((8ull << 15) * (64u / kb)); }
 
 static bool is_pow2(uint64_t x) { return x && !(x & (x - 1)); }
 

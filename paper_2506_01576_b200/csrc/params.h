@@ -146,12 +146,31 @@ cudaError_t build_bucket_index(int kb, const void* a, uint64_t n, uint32_t D, ui
                                uint64_t B, uint64_t gbase, uint32_t gsh, uint32_t* tab, uint64_t* par, uint32_t* gnode,
                                uint32_t* mx, uint16_t* dir, cudaStream_t s);
 bool bucket_workspace_bytes(uint64_t B, uint64_t m, int kb, int ob, uint32_t sm_count, uint64_t* bytes);
+// largest array a bucket index covers (two-level units of 16 leaves of 32 B)
+inline uint64_t bucket_max_keys(uint32_t kb) { return (uint64_t)kBkMaxBuckets * ((8ull << 15) * (64u / kb)); }
 // phase 0: the whole pipeline; 1: histogram + partition only (run = the partitioned
 // batch, searched by the caller into run->rp: BS_BUCKET_KARY=1 A/B runs); 2: restore
 // query order only
+// Fused peer return (bs_lookup_peer with layout.reorder = BUCKET, peer.cu): the
+// batch is this rank's receive window, its size the received count *m_dev
+// (m = min(*m_dev, m)); k_bk_unpart stores the result of window slot s,
+// globalised by + base, into ret[tag[s] >> shift][tag[s] & (2^shift - 1)] and
+// its last CTA re-arms *cursor and bumps every rank's return counter sig[r].
+struct BucketPeer {
+    const unsigned long long* m_dev = nullptr;
+    uint64_t m_hint = 0;                  // expected batch (sizes the search items)
+    const uint32_t* tag = nullptr;
+    uint64_t* const* ret = nullptr;       // [P] return windows (device array of peer pointers)
+    unsigned long long* const* sig = nullptr;   // [P] return counters
+    unsigned long long* cursor = nullptr;
+    unsigned* done = nullptr;
+    uint64_t base = 0;
+    uint32_t P = 1, shift = 32;
+};
 cudaError_t launch_bucket(int kb, int ob, const BucketIndex& bi, const void* a, uint64_t n, const void* q, uint64_t m,
                           void* out, uint32_t stream_hint, uint32_t chunk, void* ws, uint64_t ws_bytes,
-                          uint32_t sm_count, cudaStream_t s, bool* uns, int phase, BucketRun* run);
+                          uint32_t sm_count, cudaStream_t s, bool* uns, int phase, BucketRun* run,
+                          const BucketPeer* peer = nullptr);
 
 // Shared-memory carve-out of a kernel (cudaFuncAttributePreferredSharedMemoryCarveout,
 // percent of the SM's 228 KB unified L1/shared array): the smallest that holds the

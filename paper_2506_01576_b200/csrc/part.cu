@@ -41,6 +41,7 @@
 
 #include "common.cuh"
 #include "params.h"
+#include "peer_sync.cuh"
 
 namespace bs {
 
@@ -256,7 +257,16 @@ struct BkParams {
     uint16_t* bkid;          // [m] bucket of query j (k_bk_hist -> k_bk_part)
     uint32_t* trun;          // [ntiles * B] (global position of run b) - (its sorted start), mod 2^32
     uint32_t* item_ctr;      // search items handed out (zeroed before the search)
+    BucketPeer pr;           // fused peer return (pr.m_dev != NULL), params.h
 };
+
+// the batch size: m, or for the peer window the received count (capped at m)
+template <class K>
+__device__ __forceinline__ uint64_t bk_m(const BkParams<K>& p) {
+    if (!p.pr.m_dev) return p.m;
+    const uint64_t c = *(volatile const unsigned long long*)p.pr.m_dev;
+    return c < p.m ? c : p.m;
+}
 
 // bucket of x: #(bucket maxima < x).  The radix directory packs, per bin of
 // the 32-bit global image, the candidate bucket range [lo, hi] (lo | hi << 16):
@@ -388,20 +398,21 @@ k_bk_hist(const BkParams<K> p) {
     for (uint32_t b = threadIdx.x; b < p.B; b += blockDim.x) hist[b] = 0;
     __syncthreads();
     const uint64_t pol = p.stream_hint ? policy_evict_first() : policy_evict_normal();
-    const uint64_t ntiles = (p.m + T - 1) / T;
+    const uint64_t m = bk_m(p);
+    const uint64_t ntiles = (m + T - 1) / T;
     // vector loads need the batch 2-key aligned (bs_lookup only requires key alignment)
     const bool pairs_ok = ((uintptr_t)p.q & (2 * sizeof(K) - 1)) == 0;
     auto load_tile = [&](uint64_t t, K* xs) {
         const uint64_t b0 = t * T;
-        const bool full = pairs_ok && t < ntiles && b0 + T <= p.m;
+        const bool full = pairs_ok && t < ntiles && b0 + T <= m;
 #pragma unroll
         for (uint32_t e = 0; e < E2; ++e) {
             const uint64_t j = b0 + 2 * (e * kBkPThreads + threadIdx.x);
             if (full) {
                 ld_pair<K>(p.q + j, pol, xs[2 * e], xs[2 * e + 1]);
             } else {
-                xs[2 * e] = (t < ntiles && j < p.m) ? load_stream(p.q + j, true, pol) : (K)0;
-                xs[2 * e + 1] = (t < ntiles && j + 1 < p.m) ? load_stream(p.q + j + 1, true, pol) : (K)0;
+                xs[2 * e] = (t < ntiles && j < m) ? load_stream(p.q + j, true, pol) : (K)0;
+                xs[2 * e + 1] = (t < ntiles && j + 1 < m) ? load_stream(p.q + j + 1, true, pol) : (K)0;
             }
         }
     };
@@ -410,7 +421,7 @@ k_bk_hist(const BkParams<K> p) {
     if constexpr (PF) load_tile(blockIdx.x, xn);
     for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const uint64_t b0 = t * T;
-        const uint32_t cntq = (uint32_t)((p.m - b0) < T ? (p.m - b0) : T);
+        const uint32_t cntq = (uint32_t)((m - b0) < T ? (m - b0) : T);
         K x[2 * E2];
         if constexpr (PF) {
 #pragma unroll
@@ -525,7 +536,8 @@ k_bk_part(const BkParams<K> p) {
     }
     const uint64_t pol = p.stream_hint ? policy_evict_first() : policy_evict_normal();
     const uint64_t pol_run = policy_evict_normal();
-    const uint64_t ntiles = (p.m + T - 1) / T;
+    const uint64_t m = bk_m(p);
+    const uint64_t ntiles = (m + T - 1) / T;
     constexpr bool PF = E <= 8;   // the next tile in flight when the registers allow it
     K xn[PF ? E : 1];
     uint32_t bn[PF ? E : 1];
@@ -534,7 +546,7 @@ k_bk_part(const BkParams<K> p) {
 #pragma unroll
         for (uint32_t e = 0; e < E; ++e) {
             const uint64_t j = b0 + e * kBkPThreads + threadIdx.x;
-            const bool ok = t < ntiles && j < p.m;
+            const bool ok = t < ntiles && j < m;
             xs[e] = ok ? load_stream(p.q + j, true, pol) : (K)0;
             bs[e] = ok ? (uint32_t)__ldcs(p.bkid + j) : 0xFFFFu;   // from k_bk_hist
         }
@@ -542,7 +554,7 @@ k_bk_part(const BkParams<K> p) {
     if constexpr (PF) load_tile(blockIdx.x, xn, bn);
     for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const uint64_t b0 = t * T;
-        const uint32_t cntq = (uint32_t)((p.m - b0) < T ? (p.m - b0) : T);
+        const uint32_t cntq = (uint32_t)((m - b0) < T ? (m - b0) : T);
         K x[E];
         uint32_t br[E];   // bucket | rank in the tile's run << 16
         if constexpr (PF) {
@@ -857,12 +869,13 @@ k_bk_unpart(const BkParams<K> p) {
     uint32_t* rb = reinterpret_cast<uint32_t*>(so + T);       // [B]
     const uint32_t B = p.B;
     const uint64_t pol = p.stream_hint ? policy_evict_first() : policy_evict_normal();
-    const uint64_t ntiles = (p.m + T - 1) / T;
+    const uint64_t m = bk_m(p);
+    const uint64_t ntiles = (m + T - 1) / T;
     const uint64_t pol_run = policy_evict_normal();   // runs share lines with the neighbouring tiles' runs
     const O* rp = (const O*)p.rp;
     for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const uint64_t b0 = t * T;
-        const uint32_t cntq = (uint32_t)((p.m - b0) < T ? (p.m - b0) : T);
+        const uint32_t cntq = (uint32_t)((m - b0) < T ? (m - b0) : T);
         for (uint32_t b = threadIdx.x; b < B; b += blockDim.x) rb[b] = p.trun[t * B + b];
         uint32_t bp[E];   // bucket | slot << 16
 #pragma unroll
@@ -887,6 +900,22 @@ k_bk_unpart(const BkParams<K> p) {
             }
         }
         __syncthreads();
+        if constexpr (OB == 8) {
+            if (p.pr.m_dev) {
+                // fused peer return: window slot b0 + j's result, made global (+ the
+                // shard's base), straight into its source rank's return window
+                constexpr uint64_t MISS = 1ull << 63;
+                const uint32_t sh = p.pr.shift;
+                const uint64_t msk = (1ull << sh) - 1ull;
+                for (uint32_t j = threadIdx.x; j < cntq; j += blockDim.x) {
+                    const uint32_t tg = __ldcg(p.pr.tag + b0 + j);
+                    const uint64_t v = (uint64_t)so[j];
+                    const uint64_t g = (v & ~MISS) + p.pr.base;
+                    p.pr.ret[(uint64_t)tg >> sh][tg & msk] = (v & MISS) ? (g | MISS) : g;
+                }
+                continue;
+            }
+        }
         O* out = (O*)p.out + b0;
         if (cntq == T && OB == 8 && ((uintptr_t)p.out & 15) == 0) {
             // 16-B stores: two results per thread per step
@@ -898,6 +927,15 @@ k_bk_unpart(const BkParams<K> p) {
             }
         } else {
             for (uint32_t j = threadIdx.x; j < cntq; j += blockDim.x) store_stream(out + j, so[j], true, pol);
+        }
+    }
+    if constexpr (OB == 8) {
+        if (p.pr.m_dev && peer_last_cta(p.pr.done)) {
+            // every CTA has read the cursor and stored its results: re-arm the
+            // window, then tell every rank its results have landed
+            *p.pr.cursor = 0;
+            __threadfence_system();
+            for (uint32_t r = 0; r < p.pr.P; ++r) red_release_sys_add_u64(p.pr.sig[r], 1ull);
         }
     }
 }
@@ -1004,9 +1042,11 @@ static cudaError_t go_bucket(BkParams<K> p, const BkLayout& L, char* ws, cudaStr
 
 cudaError_t launch_bucket(int kb, int ob, const BucketIndex& bi, const void* a, uint64_t n, const void* q, uint64_t m,
                           void* out, uint32_t stream_hint, uint32_t chunk, void* ws, uint64_t ws_bytes,
-                          uint32_t sm_count, cudaStream_t s, bool* uns, int phase, BucketRun* run) {
+                          uint32_t sm_count, cudaStream_t s, bool* uns, int phase, BucketRun* run,
+                          const BucketPeer* peer) {
     BkLayout L;
-    if (!bi.mx || (phase == 0 && !bi.tab) || !bk_layout(bi.B, m, kb, ob, sm_count, &L) || ws_bytes < L.total) {
+    if (!bi.mx || (phase == 0 && !bi.tab) || !bk_layout(bi.B, m, kb, ob, sm_count, &L) || ws_bytes < L.total ||
+        (peer && (phase != 0 || ob != 8 || !peer->m_dev))) {
         *uns = true;
         return cudaSuccess;
     }
@@ -1015,13 +1055,15 @@ cudaError_t launch_bucket(int kb, int ob, const BucketIndex& bi, const void* a, 
         p.B = (uint32_t)bi.B; p.D = bi.D; p.NB = bi.NB; p.LB = bi.LB; p.G = bi.G;
         p.tab = bi.tab; p.par = bi.par; p.mx = bi.mx; p.dir = bi.dir; p.gnode = bi.gnode;
         p.gbase = bi.gbase; p.gsh = bi.gsh;
+        if (peer) p.pr = *peer;
+        const uint64_t mi = peer && peer->m_hint ? peer->m_hint : m;
         // search items: the CTAs' window of items spans ~37 MB of keys (config 3:
         // 37 fine buckets of 1 MB; config 4: ~2.3 two-level buckets of 16 MB),
         // at most kBkChunk (the config-3 optimum) and at least 4096 queries
         uint64_t ch = chunk;
         if (!ch) {
             const uint64_t bucket_bytes = bi.NB * (uint64_t)kb;
-            ch = (uint64_t)((double)m * (37.0 * (1 << 20) / (double)bucket_bytes) / ((double)sm_count * (double)bi.B));
+            ch = (uint64_t)((double)mi * (37.0 * (1 << 20) / (double)bucket_bytes) / ((double)sm_count * (double)bi.B));
             ch = ch > kBkChunk ? kBkChunk : (ch < 4096 ? 4096 : ch);
         }
         p.CH = (uint32_t)ch;

@@ -103,6 +103,9 @@ struct PeerState {
     uint64_t** d_ret = nullptr;      // [P]
     unsigned long long** d_sig = nullptr;   // [P] return counters
     uint64_t* d_shard_max = nullptr; // [P] (u64 storage, low kb bytes)
+    bool bucket = false;             // lookup = the BUCKET pipeline over the window (layout.reorder)
+    void* bk_ws = nullptr;           // its workspace, sized for the window (cap queries)
+    uint64_t bk_ws_bytes = 0;
     PeerCtl* ctl() const { return (PeerCtl*)region; }
 };
 
@@ -111,7 +114,7 @@ void destroy_peer_state(Index* ix) {
     if (!d) return;
     for (void* p : d->opened)
         if (p) cudaIpcCloseMemHandle(p);
-    void* bufs[] = {d->region, d->d_peers, d->d_ret, d->d_sig, d->d_shard_max};
+    void* bufs[] = {d->region, d->d_peers, d->d_ret, d->d_sig, d->d_shard_max, d->bk_ws};
     for (void* b : bufs)
         if (b) cudaFree(b);
     delete d;
@@ -193,6 +196,14 @@ __global__ void __launch_bounds__(kRouteThreads) k_peer_route(const K* __restric
 
 constexpr int kFinishUnroll = 4;
 
+// BUCKET lookup: the partition passes read the window with plain streaming
+// loads, so they must start after every rank's route has landed — this
+// one-thread kernel holds the stream until the route counter reaches target
+// (the same bounded acquire the K-ary kernel does in its prologue).
+__global__ void k_peer_wait(const unsigned long long* sig, unsigned long long target, unsigned* err) {
+    peer_wait_ge(sig, target, err);
+}
+
 __global__ void __launch_bounds__(256) k_peer_finish(const uint64_t* ret, uint64_t m, uint64_t* __restrict__ out,
                                                      const unsigned long long* ret_sig, unsigned long long target,
                                                      unsigned* err) {
@@ -251,7 +262,8 @@ int bs_build_peer(const void* local_keys, uint64_t n_local, const bs_layout* lay
     // reject, after the AUTO choices are resolved, every layout the g1 kernel cannot
     // run: a lookup would otherwise fail only after its route kernel had already
     // filled the peers' windows and bumped their counters
-    if (!g1_shape_ok(ix))
+    const bool bucket = ix->layout.reorder == BS_REORDER_BUCKET;
+    if (!bucket && !g1_shape_ok(ix))
         return cleanup(fail(BS_ERR_UNSUPPORTED, "bs_build_peer: layout needs kary_mode 6/7 with W*key <= 64 B and "
                                                 "C*key in 32..256 B (got mode %u, W %u, C %u, key %u B)",
                             ix->layout.kary_mode, ix->kW, ix->kC, ix->kb));
@@ -263,6 +275,17 @@ int bs_build_peer(const void* local_keys, uint64_t n_local, const bs_layout* lay
     d->max_m = max_m_local;
     d->cap = recv_capacity ? recv_capacity : (uint64_t)world * (max_m_local ? max_m_local : 1);
     if (d->cap >= (1ull << 40)) return cleanup(fail(BS_ERR_INVALID, "bs_build_peer: recv_capacity too large"));
+    if (bucket) {
+        // the window is partitioned in place of a caller batch: workspace for cap queries
+        if (!ix->bk.mx || !bucket_workspace_bytes(ix->bk.B, d->cap, ix->kb, 8, (uint32_t)ix->sm_count, &d->bk_ws_bytes))
+            return cleanup(fail(BS_ERR_UNSUPPORTED, "bs_build_peer: BS_REORDER_BUCKET needs n_local <= %llu keys and "
+                                                    "recv_capacity < 2^32",
+                                (unsigned long long)bucket_max_keys(ix->kb)));
+        cudaError_t e = cudaMalloc(&d->bk_ws, d->bk_ws_bytes);
+        if (e != cudaSuccess) return cleanup(fail(BS_ERR_OOM, "bs_build_peer: cudaMalloc(%llu B bucket workspace): %s",
+                                                  (unsigned long long)d->bk_ws_bytes, cudaGetErrorString(e)));
+        d->bucket = true;
+    }
     d->lay = region_layout(d->cap, d->max_m, d->kb);
     cudaError_t e = cudaMalloc(&d->region, d->lay.total);
     if (e != cudaSuccess) return cleanup(fail(BS_ERR_OOM, "bs_build_peer: cudaMalloc(%llu B window): %s",
@@ -388,7 +411,7 @@ int bs_lookup_peer(const void* idx, const void* local_queries, uint64_t m_local,
     if (m_local && !local_queries) return fail(BS_ERR_INVALID, "bs_lookup_peer: NULL queries");
     if ((uintptr_t)local_queries % ix->kb || (uintptr_t)out_local % 8)
         return fail(BS_ERR_INVALID, "bs_lookup_peer: misaligned queries/out");
-    if (!g1_shape_ok(ix)) return fail(BS_ERR_UNSUPPORTED, "bs_lookup_peer: layout cannot run the g1 kernel");
+    if (!d->bucket && !g1_shape_ok(ix)) return fail(BS_ERR_UNSUPPORTED, "bs_lookup_peer: layout cannot run the g1 kernel");
     cudaStream_t s = (cudaStream_t)stream;
     const uint32_t P = (uint32_t)d->P, me = (uint32_t)d->rank;
     PeerCtl* c = d->ctl();
@@ -411,8 +434,34 @@ int bs_lookup_peer(const void* idx, const void* local_queries, uint64_t m_local,
     // once the route kernel is queued the call is committed: every rank waits
     // for this one, so a failure past this point is fatal for the group
     d->epoch += 1;
-    int rc = dispatch_kary_peer(ix, d->region + d->lay.q, d->cap, s, L, pl);
-    if (rc != BS_OK) return rc;
+    if (d->bucket) {
+        // route -> wait -> hist / scan / part / search / unpart over the window;
+        // the unpartition stores each result into its source's return window
+        k_peer_wait<<<1, 1, 0, s>>>(&c->route_sig, target, &c->err);
+        count_launch();
+        BucketPeer bp;
+        bp.m_dev = &c->cursor;
+        bp.m_hint = d->max_m;
+        bp.tag = (const uint32_t*)(d->region + d->lay.tag);
+        bp.ret = d->d_ret;
+        bp.sig = d->d_sig;
+        bp.cursor = &c->cursor;
+        bp.done = &c->done_look;
+        bp.base = d->base[me];
+        bp.P = P;
+        bp.shift = tag_shift(P);
+        bool uns = false;
+        uint32_t chunk = 0;
+        if (const char* v = getenv("BS_BUCKET_CHUNK")) chunk = (uint32_t)atoi(v);
+        e = launch_bucket(ix->kb, 8, ix->bk, ix->d_keys, ix->n, d->region + d->lay.q, d->cap, nullptr,
+                          (L.cache_hints & BS_HINT_STREAM_EVICT_FIRST) ? 1u : 0u, chunk, d->bk_ws, d->bk_ws_bytes,
+                          (uint32_t)ix->sm_count, s, &uns, 0, nullptr, &bp);
+        if (uns) return fail(BS_ERR_UNSUPPORTED, "bs_lookup_peer: bucket pipeline cannot run this window");
+        if (e != cudaSuccess) return fail_cuda(e, "bs_lookup_peer: bucket pipeline launch");
+    } else {
+        int rc = dispatch_kary_peer(ix, d->region + d->lay.q, d->cap, s, L, pl);
+        if (rc != BS_OK) return rc;
+    }
     // out_local == NULL: the results stay in the return window (bs_peer_results)
     const uint64_t mc = out_local ? m_local : 0;
     k_peer_finish<<<grid_for(mc / 2, (unsigned)ix->sm_count * 8), 256, 0, s>>>(

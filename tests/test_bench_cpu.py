@@ -122,4 +122,4 @@ def test_default_reorder_per_config():
     assert bench.default_reorder("config3", "sorted") == 3
     assert bench.default_reorder("config2", "random") == 0
     assert bench.default_reorder("config1", "random") == 0
-    assert bench.default_reorder("config5", "random") == 0
+    assert bench.default_reorder("config5", "random") == 5

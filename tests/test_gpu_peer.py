@@ -25,8 +25,8 @@ import paper_2506_01576_b200 as P  # noqa: E402
 from paper_2506_01576_b200 import bs  # noqa: E402
 
 
-def _layout(kb):
-    return bs.bs_layout_default(key_bytes=kb, out_bytes=8, variant=bs.KARY)
+def _layout(kb, reorder=0):
+    return bs.bs_layout_default(key_bytes=kb, out_bytes=8, variant=bs.KARY, reorder=reorder)
 
 
 @pytest.mark.parametrize("kb", [8, 4])
@@ -51,6 +51,53 @@ def test_peer_world1(kb):
     assert np.array_equal(P.to_numpy_unsigned(out[1:1 + q.size], 8), oracle.lookup(keys, q, out_bytes=8))
     err, calls = bs.bs_peer_status(idx)
     assert err == 0 and calls == 6
+    idx.close()
+
+
+@pytest.mark.parametrize("kb,n", [(8, 200003), (4, 200003), (8, 3 << 20), (4, 5 << 20)])
+def test_peer_world1_bucket(kb, n):
+    """layout.reorder = BUCKET: the window is partitioned and searched by the
+    bucket pipeline (part.cu), whose unpartition stores every result into its
+    source's return window; m spans several 8192-query tiles with ragged tails,
+    one bucket (n = 200003) and several (3 / 5 Mi keys), across calls (the
+    cursor re-arm and the monotonic counters)."""
+    keys = workload.gen_keys(n, kb, seed=23)
+    idx = bs.bs_build_peer(P.as_torch(keys), keys.size, _layout(kb, bs.REORDER_BUCKET), 0, 1, 300000)
+    bs.bs_peer_connect(idx, [bs.bs_peer_export(idx)])
+    out = torch.empty(300000, dtype=torch.int64, device="cuda")
+    for call, (m, hr) in enumerate([(300000, 0.6), (0, 1.0), (1, 0.0), (8192, 1.0), (12345, 1.0), (299999, 0.3)]):
+        q = workload.gen_queries(keys, max(m, 1), seed=200 + call, hit_ratio=hr)[:m]
+        bs.bs_lookup_peer(idx, P.as_torch(q) if m else None, m, out)
+        torch.cuda.synchronize()
+        if m:
+            got = P.to_numpy_unsigned(out[:m], 8)
+            want = oracle.lookup(keys, q, out_bytes=8)
+            assert np.array_equal(got, want), f"call {call}: first mismatch at {np.flatnonzero(got != want)[:5]}"
+    err, calls = bs.bs_peer_status(idx)
+    assert err == 0 and calls == 6
+    idx.close()
+
+
+def test_peer_bucket_results_window_and_overflow():
+    keys = workload.gen_keys(1 << 20, 8, seed=43)
+    idx = bs.bs_build_peer(P.as_torch(keys), keys.size, _layout(8, bs.REORDER_BUCKET), 0, 1, 50000)
+    bs.bs_peer_connect(idx, [bs.bs_peer_export(idx)])
+    q = workload.gen_queries(keys, 50000, seed=44, hit_ratio=0.5)
+    bs.bs_lookup_peer(idx, P.as_torch(q), q.size, None)
+    torch.cuda.synchronize()
+    win = torch.as_tensor(_DeviceWindow(bs.bs_peer_results(idx), q.size), device="cuda")
+    assert np.array_equal(P.to_numpy_unsigned(win, 8), oracle.lookup(keys, q, out_bytes=8))
+    assert bs.bs_peer_status(idx)[0] == 0
+    idx.close()
+    # a window smaller than the batch: flagged, the received prefix still looked up
+    idx = bs.bs_build_peer(P.as_torch(keys), keys.size, _layout(8, bs.REORDER_BUCKET), 0, 1, 20000,
+                           recv_capacity=9000)
+    bs.bs_peer_connect(idx, [bs.bs_peer_export(idx)])
+    q = workload.gen_queries(keys, 20000, seed=45)
+    out = torch.empty(20000, dtype=torch.int64, device="cuda")
+    bs.bs_lookup_peer(idx, P.as_torch(q), q.size, out)
+    torch.cuda.synchronize()
+    assert bs.bs_peer_status(idx)[0] & 1
     idx.close()
 
 
@@ -102,14 +149,14 @@ def _free_port():
     return p
 
 
-def _world2_worker(rank, world, port, keys, cut, calls, ret, kb=8):
+def _world2_worker(rank, world, port, keys, cut, calls, ret, kb=8, reorder=0):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.cuda.set_device(rank)   # one process per GPU (ranks that wait on each other must not share one)
     shard = keys[:cut] if rank == 0 else keys[cut:]
     max_m = max(m for m, _ in calls)
-    idx = bs.bs_build_peer(P.as_torch(shard), shard.size, _layout(kb), rank, world, max_m)
+    idx = bs.bs_build_peer(P.as_torch(shard), shard.size, _layout(kb, reorder), rank, world, max_m)
     bs.bs_peer_connect_group(idx)
     out = torch.empty(max_m, dtype=torch.int64, device="cuda")
     res = []
@@ -127,8 +174,8 @@ def _world2_worker(rank, world, port, keys, cut, calls, ret, kb=8):
 
 
 @pytest.mark.timeout(600)
-@pytest.mark.parametrize("kb", [8, 4])
-def test_peer_world2(kb):
+@pytest.mark.parametrize("kb,reorder", [(8, 0), (4, 0), (8, 5), (4, 5)])
+def test_peer_world2(kb, reorder):
     """World 2, one process per GPU.  Needs two GPUs: B200_PROFILING.md forbids
     running ranks whose kernels wait on each other as processes on ONE GPU
     (Xid 109 seen with 2-4 such ranks), which round 1 did; the rank logic is
@@ -144,7 +191,7 @@ def test_peer_world2(kb):
     ctx = mp.get_context("spawn")
     mgr = ctx.Manager()
     ret = mgr.dict()
-    mp.start_processes(_world2_worker, args=(2, _free_port(), keys, cut, calls, ret, kb), nprocs=2, join=True,
+    mp.start_processes(_world2_worker, args=(2, _free_port(), keys, cut, calls, ret, kb, reorder), nprocs=2, join=True,
                        start_method="spawn")
     for r in range(2):
         res, err = ret[r]

@@ -22,6 +22,9 @@ KEYS = {   # run name -> (traffic key, queries per launch, kernels of one step)
                  ["k_bk_hist", "k_bk_scan", "k_bk_part", "k_bk_search", "k_bk_unpart"]),
     "c4bucket": ("config4/random/kary/K5/C16/mode7/r5", 1 << 30,
                  ["k_bk_hist", "k_bk_scan", "k_bk_part", "k_bk_search", "k_bk_unpart"]),
+    "c5bucket": ("config5/random/kary/K5/C16/mode7/peer/r5", 1 << 28,
+                 ["k_peer_route", "k_peer_wait", "k_bk_hist", "k_bk_scan", "k_bk_part", "k_bk_search", "k_bk_unpart",
+                  "k_peer_finish"]),
 }
 
 
