@@ -396,7 +396,12 @@ void bs_dist_destroy(void* comm);
 #define BS_PEER_BLOB_BYTES 256
 
 /* Builds this rank's index over its local ascending keys (device pointer,
- * n_local >= 1; layout must give variant KARY and out_bytes 8) and allocates
+ * n_local >= 1; layout must give variant KARY and out_bytes 8; layout.reorder
+ * = BS_REORDER_BUCKET makes the owner look its receive window up with the
+ * key-range partition pipeline, whose unpartition stores the results into
+ * the sources' return windows — workspace for recv_capacity queries is
+ * allocated here, n_local must fit a bucket index and recv_capacity < 2^32;
+ * any other reorder runs the K-ary kernel's peer epilogue) and allocates
  * its IPC-exportable window: receive slots (recv_capacity keys + 4-B return
  * tags, (src_rank << (32 - ceil(log2 world))) | src_idx; recv_capacity 0 =
  * world * max_m_local, which can never overflow) and a return window of

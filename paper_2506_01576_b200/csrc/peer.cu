@@ -17,6 +17,12 @@
 //                  kept) straight into the source rank's return window at the
 //                  source index.  The last CTA re-arms the cursor and bumps
 //                  every rank's return counter.
+//   (BUCKET)       with layout.reorder = BS_REORDER_BUCKET, k_peer_wait holds
+//                  the stream for the route counter and the part.cu pipeline
+//                  (hist / scan / part / search / unpart) runs over the window,
+//                  its size read from the cursor on the device; the unpartition
+//                  stores each result into the source's return window and its
+//                  last CTA re-arms the cursor and signals, as above.
 //   k_peer_finish  waits for its return counter to reach t*P, copies the
 //                  return window to the caller's out (or leaves the results
 //                  in the window: out_local == NULL, bs_peer_results).
