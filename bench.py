@@ -627,8 +627,25 @@ def main():
         for _ in range(e2e_steps):
             e2e_step()
         dt = reduce_max([(time.perf_counter() - t0) / e2e_steps], world, "cuda")[0]
+        # the PCIe floor of the same bytes: the step's H2D and D2H copies alone,
+        # concurrently on two streams (the link is full duplex), no lookup
+        s2 = torch.cuda.Stream()
+
+        def copies():
+            with torch.cuda.stream(stream):
+                dq.copy_(hq, non_blocking=True)   # same values: dq is hq's source
+            with torch.cuda.stream(s2):
+                hout.copy_(out, non_blocking=True)
+            stream.synchronize()
+            s2.synchronize()
+        copies()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            copies()
+        dcp = reduce_max([(time.perf_counter() - t0) / e2e_steps], world, "cuda")[0]
         e2e = {"value": m_job / dt, "unit": "lookups/s", "h2d_bytes_per_step": m * kb,
-               "d2h_bytes_per_step": m * ob, "ms_per_step": dt * 1e3, "api": api}
+               "d2h_bytes_per_step": m * ob, "ms_per_step": dt * 1e3, "api": api,
+               "pcie_floor_ms": dcp * 1e3, "frac_of_pcie_floor": dcp / dt}
         del hq, hout
 
     # ---- roofline ----
