@@ -260,12 +260,17 @@ struct BkParams {
     BucketPeer pr;           // fused peer return (pr.m_dev != NULL), params.h
 };
 
-// the batch size: m, or for the peer window the received count (capped at m)
-template <class K>
+// the batch size: m, or for the peer window (PM) the received count (capped
+// at m).  A compile-time choice: a run-time one keeps m in registers for the
+// whole kernel (measured: an 8-B spill in k_bk_part, +6 % on that pass)
+template <bool PM, class K>
 __device__ __forceinline__ uint64_t bk_m(const BkParams<K>& p) {
-    if (!p.pr.m_dev) return p.m;
-    const uint64_t c = *(volatile const unsigned long long*)p.pr.m_dev;
-    return c < p.m ? c : p.m;
+    if constexpr (!PM) {
+        return p.m;
+    } else {
+        const uint64_t c = *(volatile const unsigned long long*)p.pr.m_dev;
+        return c < p.m ? c : p.m;
+    }
 }
 
 // bucket of x: #(bucket maxima < x).  The radix directory packs, per bin of
@@ -385,7 +390,7 @@ __device__ __forceinline__ void ld_pair(const K* p, uint64_t pol, K& x0, K& x1) 
 // tile's queries are in flight while this tile is bucketed.  Each thread takes
 // pairs of neighbouring queries (one vector load, one 4-B store of the two
 // bucket ids): the pass is issue-bound, not bandwidth-bound.
-template <class K>
+template <class K, bool PM>
 __global__ void __launch_bounds__(kBkPThreads, kBkPCtas)
 k_bk_hist(const BkParams<K> p) {
     constexpr uint32_t T = kBkTile, E2 = T / kBkPThreads / 2;   // pairs per thread per tile
@@ -398,7 +403,7 @@ k_bk_hist(const BkParams<K> p) {
     for (uint32_t b = threadIdx.x; b < p.B; b += blockDim.x) hist[b] = 0;
     __syncthreads();
     const uint64_t pol = p.stream_hint ? policy_evict_first() : policy_evict_normal();
-    const uint64_t m = bk_m(p);
+    const uint64_t m = bk_m<PM>(p);
     const uint64_t ntiles = (m + T - 1) / T;
     // vector loads need the batch 2-key aligned (bs_lookup only requires key alignment)
     const bool pairs_ok = ((uintptr_t)p.q & (2 * sizeof(K) - 1)) == 0;
@@ -491,7 +496,7 @@ k_bk_scan(uint32_t* __restrict__ cnt, uint32_t* __restrict__ tot, uint32_t G, ui
 // costs four barriers (ranks / warp totals / run starts / sorted tile) and no
 // loops over the buckets; the next tile's queries and bucket ids are in flight
 // while this tile is sorted and stored.
-template <class K>
+template <class K, bool PM>
 __global__ void __launch_bounds__(kBkPThreads, kBkPCtas)
 k_bk_part(const BkParams<K> p) {
     constexpr uint32_t T = kBkTile, E = T / kBkPThreads, BPT = kBkFineMax / kBkPThreads;
@@ -536,8 +541,18 @@ k_bk_part(const BkParams<K> p) {
     }
     const uint64_t pol = p.stream_hint ? policy_evict_first() : policy_evict_normal();
     const uint64_t pol_run = policy_evict_normal();
-    const uint64_t m = bk_m(p);
-    const uint64_t ntiles = (m + T - 1) / T;
+    // PM: the received count is re-read from shared memory at each use — held
+    // in registers across the kernel it costs an 8-B spill (64 registers)
+    __shared__ unsigned long long s_m;
+    if constexpr (PM) {
+        if (threadIdx.x == 0) s_m = bk_m<true>(p);
+        __syncthreads();
+    }
+    auto M = [&]() -> uint64_t {
+        if constexpr (PM) return *(volatile unsigned long long*)&s_m;
+        else return p.m;
+    };
+    const uint64_t ntiles = (M() + T - 1) / T;
     constexpr bool PF = E <= 8;   // the next tile in flight when the registers allow it
     K xn[PF ? E : 1];
     uint32_t bn[PF ? E : 1];
@@ -546,7 +561,7 @@ k_bk_part(const BkParams<K> p) {
 #pragma unroll
         for (uint32_t e = 0; e < E; ++e) {
             const uint64_t j = b0 + e * kBkPThreads + threadIdx.x;
-            const bool ok = t < ntiles && j < m;
+            const bool ok = t < ntiles && j < M();
             xs[e] = ok ? load_stream(p.q + j, true, pol) : (K)0;
             bs[e] = ok ? (uint32_t)__ldcs(p.bkid + j) : 0xFFFFu;   // from k_bk_hist
         }
@@ -554,7 +569,7 @@ k_bk_part(const BkParams<K> p) {
     if constexpr (PF) load_tile(blockIdx.x, xn, bn);
     for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const uint64_t b0 = t * T;
-        const uint32_t cntq = (uint32_t)((m - b0) < T ? (m - b0) : T);
+        const uint32_t cntq = (uint32_t)((M() - b0) < T ? (M() - b0) : T);
         K x[E];
         uint32_t br[E];   // bucket | rank in the tile's run << 16
         if constexpr (PF) {
@@ -859,7 +874,7 @@ k_bk_search(const BkParams<K> p) {
 }
 
 // ---- pass 5: back to query order (any grid: the run bases are stored per tile)
-template <class K, int OB>
+template <class K, int OB, bool PM>
 __global__ void __launch_bounds__(kBkPThreads, kBkUCtas)
 k_bk_unpart(const BkParams<K> p) {
     using O = typename std::conditional<OB == 8, uint64_t, uint32_t>::type;
@@ -869,7 +884,7 @@ k_bk_unpart(const BkParams<K> p) {
     uint32_t* rb = reinterpret_cast<uint32_t*>(so + T);       // [B]
     const uint32_t B = p.B;
     const uint64_t pol = p.stream_hint ? policy_evict_first() : policy_evict_normal();
-    const uint64_t m = bk_m(p);
+    const uint64_t m = bk_m<PM>(p);
     const uint64_t ntiles = (m + T - 1) / T;
     const uint64_t pol_run = policy_evict_normal();   // runs share lines with the neighbouring tiles' runs
     const O* rp = (const O*)p.rp;
@@ -900,8 +915,8 @@ k_bk_unpart(const BkParams<K> p) {
             }
         }
         __syncthreads();
-        if constexpr (OB == 8) {
-            if (p.pr.m_dev) {
+        if constexpr (PM && OB == 8) {
+            {
                 // fused peer return: window slot b0 + j's result, made global (+ the
                 // shard's base), straight into its source rank's return window
                 constexpr uint64_t MISS = 1ull << 63;
@@ -929,8 +944,8 @@ k_bk_unpart(const BkParams<K> p) {
             for (uint32_t j = threadIdx.x; j < cntq; j += blockDim.x) store_stream(out + j, so[j], true, pol);
         }
     }
-    if constexpr (OB == 8) {
-        if (p.pr.m_dev && peer_last_cta(p.pr.done)) {
+    if constexpr (PM && OB == 8) {
+        if (peer_last_cta(p.pr.done)) {
             // every CTA has read the cursor and stored its results: re-arm the
             // window, then tell every rank its results have landed
             *p.pr.cursor = 0;
@@ -1002,19 +1017,20 @@ static cudaError_t go_bucket(BkParams<K> p, const BkLayout& L, char* ws, cudaStr
     p.trun = (uint32_t*)(ws + L.o_trun);
     p.item_ctr = (uint32_t*)(ws + L.o_ctr);
     if (run) { run->rq = p.rq; run->rp = p.rp; }
+    const bool pm = p.pr.m_dev != nullptr;   // the peer window (size on the device)
     const uint32_t B = p.B, B4 = (B + 3u) & ~3u;
     cudaError_t e;
     if (phase != 2) {
         {
             const uint32_t smem = 8u * B4 + 4u * kBkBins;
-            e = bk_launch((const void*)k_bk_hist<K>, kBkPThreads, smem, p.Gp, &p, s);
+            e = bk_launch(pm ? (const void*)k_bk_hist<K, true> : (const void*)k_bk_hist<K, false>, kBkPThreads, smem, p.Gp, &p, s);
             if (e != cudaSuccess) return e;
         }
         k_bk_scan<<<(B + 31) / 32, 1024, 0, s>>>(p.cnt, p.tot, p.Gp, B);
         count_launch();
         {
             const uint32_t smem = kBkTile * ((uint32_t)sizeof(K) + 4u) + 4u * (3u * kBkFineMax + 32u);
-            e = bk_launch((const void*)k_bk_part<K>, kBkPThreads, smem, p.Gp, &p, s);
+            e = bk_launch(pm ? (const void*)k_bk_part<K, true> : (const void*)k_bk_part<K, false>, kBkPThreads, smem, p.Gp, &p, s);
             if (e != cudaSuccess) return e;
         }
     }
@@ -1034,7 +1050,11 @@ static cudaError_t go_bucket(BkParams<K> p, const BkLayout& L, char* ws, cudaStr
     }
     if (phase != 1) {
         const uint32_t smem = kBkTile * OB + 4u * B4;
-        e = bk_launch((const void*)k_bk_unpart<K, OB>, kBkPThreads, smem, kBkUCtas * p.Gs, &p, s);
+        const void* ku = (const void*)k_bk_unpart<K, OB, false>;
+        if constexpr (OB == 8) {
+            if (pm) ku = (const void*)k_bk_unpart<K, 8, true>;   // the peer return (out_bytes 8 only)
+        }
+        e = bk_launch(ku, kBkPThreads, smem, kBkUCtas * p.Gs, &p, s);
         if (e != cudaSuccess) return e;
     }
     return cudaGetLastError();
