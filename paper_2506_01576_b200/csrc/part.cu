@@ -322,6 +322,22 @@ __device__ __forceinline__ uint32_t bk_bucket(const BkParams<K>& p, const uint32
     return l;
 }
 
+// The common case of bk_bucket without branches: the bin's first candidate
+// maximum decides unless the bin holds another maximum below x or an image
+// ties x's; *rare is set for those, which the caller re-resolves with bk_bucket.
+template <class K>
+__device__ __forceinline__ uint32_t bk_bucket_fast(const BkParams<K>& p, const uint32_t* MS, const uint32_t* DIR,
+                                                   K x, bool& rare) {
+    const uint32_t fx = bk_img((uint64_t)x, p.gbase, p.gsh);
+    const uint32_t w = DIR[fx >> (32 - kBkBinsLog2)];
+    const uint32_t l = w & 0xFFFFu, h = w >> 16;
+    const uint32_t v = MS[l];   // l <= B - 1: always a maximum
+    const bool has = l < h;
+    const bool lt = has && v < fx;
+    rare = (lt && l + 1 < h) || (has && v == fx);
+    return l + (lt ? 1u : 0u);
+}
+
 // stage the bucket maxima images and the packed directory (plain loads; once per CTA)
 template <class K>
 __device__ __forceinline__ void bk_stage_dir(const BkParams<K>& p, uint32_t* MS, uint32_t* DIR) {
@@ -434,6 +450,27 @@ k_bk_hist(const BkParams<K> p) {
             load_tile(t + gridDim.x, xn);
         } else {
             load_tile(t, x);
+        }
+        if (cntq == T) {
+            // full tile: each pair's buckets branch-free, a pair with a rare query
+            // (a second maximum in the bin, an image tie) re-resolved exactly —
+            // the pass is issue-bound, and branches per query cost reconvergences
+#pragma unroll
+            for (uint32_t e = 0; e < E2; ++e) {
+                const uint32_t j = 2 * (e * kBkPThreads + threadIdx.x);
+                bool r0, r1;
+                uint32_t b0v = bk_bucket_fast(p, MS, DIR, x[2 * e], r0);
+                uint32_t b1v = bk_bucket_fast(p, MS, DIR, x[2 * e + 1], r1);
+                if (__builtin_expect(r0 || r1, 0)) {
+                    b0v = bk_bucket(p, MS, DIR, x[2 * e]);
+                    b1v = bk_bucket(p, MS, DIR, x[2 * e + 1]);
+                }
+                atomicAdd(&hist[b0v], 1u);
+                atomicAdd(&hist[b1v], 1u);
+                // the partition pass reads the bucket ids back
+                __stcs(reinterpret_cast<uint32_t*>(p.bkid + b0 + j), b0v | (b1v << 16));
+            }
+            continue;
         }
 #pragma unroll
         for (uint32_t e = 0; e < E2; ++e) {
