@@ -170,14 +170,18 @@ __device__ __forceinline__ uint64_t enc(uint64_t lb, bool hit) {
     return hit ? lb : (lb | MISS);
 }
 
-template <class K, int D, int OB>
+// DB: two segment buffers — segment b+1 is staged into the other buffer while
+// b is searched, one barrier per segment instead of two (a warp that finishes
+// its queries of b stages b+1 instead of waiting at a barrier)
+template <class K, int D, int OB, bool DB>
 __global__ void __launch_bounds__(1024, 1)
 k_seg_sorted(const SegParams<K> p) {
     constexpr uint32_t S = 1u << D;
+    constexpr uint32_t NBUF = DB ? 2u : 1u;
     extern __shared__ __align__(16) uint32_t sm[];
-    uint32_t* F = sm;                                         // slot 0: segment max; 1..S-1: Eytzinger
-    K* SK = reinterpret_cast<K*>(sm + S);                     // [S] the segment's keys (the candidate reads)
-    uint64_t* bnd = reinterpret_cast<uint64_t*>(SK + S);      // query ranges of this CTA's segments
+    uint32_t* F0 = sm;                                        // [NBUF][S] slot 0: segment max; 1..S-1: Eytzinger
+    K* SK0 = reinterpret_cast<K*>(sm + NBUF * S);             // [NBUF][S] the segment's keys (the candidate reads)
+    uint64_t* bnd = reinterpret_cast<uint64_t*>(SK0 + NBUF * S);   // query ranges of this CTA's segments
     const uint64_t G = gridDim.x, B = p.B, n = p.n, m = p.m;
     const uint64_t b0 = B * blockIdx.x / G, b1 = B * (blockIdx.x + 1) / G;
     const uint32_t nb = (uint32_t)(b1 - b0);
@@ -201,18 +205,14 @@ k_seg_sorted(const SegParams<K> p) {
             nk[k] = i < len ? ldg(p.a + lo + i) : (K)0;
         }
     };
-    load_keys(b0);
-    for (uint64_t b = b0; b < b1; ++b) {
+    // segment b's image and keys from the registers into buffer `buf`
+    auto stage = [&](uint32_t buf, uint64_t b, const K* kk) {
         const uint64_t lo = b * S;
         const uint32_t len = (uint32_t)((n - lo) < S ? (n - lo) : S);
-        const K* seg = p.a + lo;
-        const K smin = ldg(seg), smax = ldg(seg + len - 1);
+        const K smin = ldg(p.a + lo), smax = ldg(p.a + lo + len - 1);
         const uint32_t sh = image_shift(smin, smax);
-        K kk[KPT];
-#pragma unroll
-        for (uint32_t k = 0; k < KPT; ++k) kk[k] = nk[k];
-        load_keys(b + 1);
-        __syncthreads();   // previous segment's searches are done with F (and bnd is written)
+        uint32_t* F = F0 + buf * S;
+        K* SK = SK0 + buf * S;
 #pragma unroll
         for (uint32_t k = 0; k < KPT; ++k) {
             const uint32_t i = k * 1024u + threadIdx.x;
@@ -220,7 +220,44 @@ k_seg_sorted(const SegParams<K> p) {
             F[i == S - 1 ? 0u : eytz_slot<D>(i)] = f;
             SK[i] = kk[k];
         }
-        __syncthreads();
+    };
+    load_keys(b0);
+    if constexpr (DB) {
+        if (b0 < b1) {
+            K kk[KPT];
+#pragma unroll
+            for (uint32_t k = 0; k < KPT; ++k) kk[k] = nk[k];
+            load_keys(b0 + 1);
+            stage(0, b0, kk);
+        }
+        __syncthreads();   // segment b0 staged (and bnd written)
+    }
+    for (uint64_t b = b0; b < b1; ++b) {
+        const uint64_t lo = b * S;
+        const uint32_t len = (uint32_t)((n - lo) < S ? (n - lo) : S);
+        const K smin = ldg(p.a + lo), smax = ldg(p.a + lo + len - 1);
+        const uint32_t sh = image_shift(smin, smax);
+        const uint32_t cur = DB ? (uint32_t)((b - b0) & 1u) : 0u;
+        if constexpr (DB) {
+            if (b + 1 < b1) {
+                // the other buffer was last read for segment b-1, before the barrier
+                K kk[KPT];
+#pragma unroll
+                for (uint32_t k = 0; k < KPT; ++k) kk[k] = nk[k];
+                load_keys(b + 2);
+                stage(cur ^ 1u, b + 1, kk);
+            }
+        } else {
+            K kk[KPT];
+#pragma unroll
+            for (uint32_t k = 0; k < KPT; ++k) kk[k] = nk[k];
+            load_keys(b + 1);
+            __syncthreads();   // previous segment's searches are done with F (and bnd is written)
+            stage(0, b, kk);
+            __syncthreads();
+        }
+        const uint32_t* F = F0 + cur * S;
+        const K* SK = SK0 + cur * S;
         const K lower = b ? ldg(p.a + lo - 1) : (K)0;
         const bool first = b == 0, last = b == B - 1;
         const uint64_t q0 = bnd[b - b0], q1 = bnd[b - b0 + 1];
@@ -265,6 +302,7 @@ k_seg_sorted(const SegParams<K> p) {
                 else store_stream((uint32_t*)p.out + ir, (uint32_t)res, true, pol_stream);
             }
         }
+        if constexpr (DB) __syncthreads();   // b+1 staged; every search of b is done with buffer cur
     }
 }
 
@@ -698,21 +736,24 @@ k_unpart(const PartParams<K> p) {
 
 // ---------------------------------------------------------------- launchers
 
-static uint64_t seg_smem_bytes(uint64_t n, uint32_t grid, uint32_t kb) {
+static uint64_t seg_smem_bytes(uint64_t n, uint32_t grid, uint32_t kb, uint32_t nbuf = 1) {
     const uint64_t S = 1ull << kSegLog2;
     const uint64_t B = (n + S - 1) / S;
     const uint64_t nb = (B + grid - 1) / grid + 1;
-    return S * (4 + kb) + nb * 8 + 16;
+    return nbuf * S * (4 + kb) + nb * 8 + 16;
 }
+constexpr uint64_t kSegSmemMax = 200u * 1024u;
 
 template <class K, int D, int OB>
 static cudaError_t go_seg(const SegParams<K>& p, Grid grid, cudaStream_t s, bool* uns) {
-    auto kern = k_seg_sorted<K, D, OB>;
+    // two segment buffers when they fit (DB), else one
+    const bool db = seg_smem_bytes(p.n, grid.sm_count, (uint32_t)sizeof(K), 2) <= kSegSmemMax;
+    auto kern = db ? k_seg_sorted<K, D, OB, true> : k_seg_sorted<K, D, OB, false>;
     const uint32_t threads = 1024;
     uint64_t g = 0;
     grid.sched_static = 1;
     grid.ctas_per_sm = 1;
-    const uint32_t smem = (uint32_t)seg_smem_bytes(p.n, grid.sm_count, (uint32_t)sizeof(K));
+    const uint32_t smem = (uint32_t)seg_smem_bytes(p.n, grid.sm_count, (uint32_t)sizeof(K), db ? 2u : 1u);
     cudaError_t e = plan_grid((const void*)kern, threads, smem, grid, grid.sm_count, carveout_for(smem, threads), &g, uns);
     if (e != cudaSuccess || *uns) return e;
     kern<<<(unsigned)g, threads, smem, s>>>(p);
@@ -724,7 +765,7 @@ cudaError_t launch_seg_sorted(int kb, int ob, const void* a, uint64_t n, const v
                               uint32_t stream_hint, Grid grid, cudaStream_t s, bool* uns) {
     constexpr int D = kSegLog2;
     const uint64_t S = 1ull << D;
-    if (seg_smem_bytes(n, grid.sm_count, (uint32_t)kb) > 200u * 1024u) { *uns = true; return cudaSuccess; }
+    if (seg_smem_bytes(n, grid.sm_count, (uint32_t)kb) > kSegSmemMax) { *uns = true; return cudaSuccess; }
     if (kb == 8) {
         SegParams<uint64_t> p{(const uint64_t*)a, n, (const uint64_t*)q, m, out, (uint32_t)ob, (n + S - 1) / S, stream_hint};
         return ob == 8 ? go_seg<uint64_t, D, 8>(p, grid, s, uns) : go_seg<uint64_t, D, 4>(p, grid, s, uns);
