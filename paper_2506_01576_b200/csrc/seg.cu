@@ -46,6 +46,7 @@
 //   k_unpart   per tile: res2 and slot2 in, results scattered back to query
 //              order in shared memory, one coalesced store (Listing 2 l.35-39's
 //              "unsort", at batch scale).
+#include <cstdlib>
 #include <cstring>
 #include <type_traits>
 
@@ -170,12 +171,14 @@ __device__ __forceinline__ uint64_t enc(uint64_t lb, bool hit) {
     return hit ? lb : (lb | MISS);
 }
 
-// DB: two segment buffers — segment b+1 is staged into the other buffer while
-// b is searched, one barrier per segment instead of two (a warp that finishes
+// SORTED, few queries per key (m < 8 n): per query a descent of the segment's
+// 32-bit image tree (Eytzinger order, D levels) + one candidate read.  DB: two
+// segment buffers — segment b+1 is staged into the other buffer while b is
+// searched, one barrier per segment instead of two (a warp that finishes
 // its queries of b stages b+1 instead of waiting at a barrier)
 template <class K, int D, int OB, bool DB>
 __global__ void __launch_bounds__(1024, 1)
-k_seg_sorted(const SegParams<K> p) {
+k_seg_sorted_eytz(const SegParams<K> p) {
     constexpr uint32_t S = 1u << D;
     constexpr uint32_t NBUF = DB ? 2u : 1u;
     extern __shared__ __align__(16) uint32_t sm[];
@@ -303,6 +306,151 @@ k_seg_sorted(const SegParams<K> p) {
             }
         }
         if constexpr (DB) __syncthreads();   // b+1 staged; every search of b is done with buffer cur
+    }
+}
+
+// #(c < h : k[c] < x) over a sorted run in shared memory, starting from the
+// bracket [l, h] that holds the answer
+template <class K>
+__device__ __forceinline__ uint32_t smem_lower_bound(const K* k, uint32_t l, uint32_t h, K x) {
+    while (l < h) {
+        const uint32_t mid = (l + h) >> 1;
+        if (k[mid] < x) l = mid + 1;
+        else h = mid;
+    }
+    return l;
+}
+
+// SORTED.  Per segment the CTA stages the segment's keys in shared memory
+// (two buffers filled by TMA bulk copies: segment b+1 lands while b is
+// searched, one barrier per segment).  The segment's queries, in blocks of 32,
+// are split evenly over the 32 warps.  Per round of up to 31 blocks, lane l
+// finds the exact position of block l's first query by bisection over the
+// staged keys (lane 31 of a full round: the next block's) — one bisection per
+// 32 queries; then every query of block j that lies between block j's and
+// block j+1's first queries (always, for an ordered batch) bisects only the
+// bracket between their positions (~log2(32 n / m) steps, the same for the
+// whole warp).  A query outside its bracket or its segment's key range (an
+// unordered batch) takes a plain bisection of the segment or of the array:
+// correct in any order, fast when ordered.
+constexpr uint32_t kSegInFlight = 8;   // blocks of 32 queries loaded ahead per warp
+
+template <class K, int D, int OB>
+__global__ void __launch_bounds__(1024, 1)
+k_seg_sorted(const SegParams<K> p) {
+    constexpr uint32_t S = 1u << D;
+    extern __shared__ __align__(16) uint32_t sm[];
+    K* SK0 = reinterpret_cast<K*>(sm);                          // [2][S] the segment's keys
+    uint64_t* bnd = reinterpret_cast<uint64_t*>(SK0 + 2 * S);   // query ranges of this CTA's segments
+    const uint64_t G = gridDim.x, B = p.B, n = p.n, m = p.m;
+    const uint64_t b0 = B * blockIdx.x / G, b1 = B * (blockIdx.x + 1) / G;
+    const uint32_t nb = (uint32_t)(b1 - b0);
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t pol_stream = p.stream_hint ? policy_evict_first() : policy_evict_normal();
+
+    uint64_t* bar = bnd + nb + 1;   // [2] one mbarrier per buffer
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
+    }
+    for (uint32_t i = threadIdx.x; i <= nb; i += blockDim.x) {
+        const uint64_t b = b0 + i;
+        bnd[i] = b == 0 ? 0 : b >= B ? m : upper_bound_any(p.q, m, ldg(p.a + b * S - 1));
+    }
+    // segment b's keys into buffer buf: a TMA bulk copy issued by thread 0,
+    // completed on the buffer's mbarrier (no registers held, the copy overlaps
+    // the search of the other buffer); a byte count that is not a multiple of
+    // 16 (only the array's last segment) is copied by all threads instead
+    auto seg_len = [&](uint64_t b) -> uint32_t {
+        const uint64_t lo = b * S;
+        return (uint32_t)((n - lo) < S ? (n - lo) : S);
+    };
+    const bool a16 = ((uintptr_t)p.a & 15u) == 0u;
+    auto bulk_ok = [&](uint64_t b) { return a16 && (seg_len(b) * (uint32_t)sizeof(K)) % 16u == 0u; };
+    auto stage = [&](uint32_t buf, uint64_t b) {
+        K* dst = SK0 + buf * S;
+        const K* src = p.a + b * S;
+        const uint32_t len = seg_len(b);
+        if (bulk_ok(b)) {
+            if (threadIdx.x == 0) {
+                const uint32_t bytes = len * (uint32_t)sizeof(K);
+                mbar_arrive_expect_tx(&bar[buf], bytes);
+                for (uint32_t o = 0; o < bytes; o += 32768u)
+                    bulk_g2s((char*)dst + o, (const char*)src + o, bytes - o < 32768u ? bytes - o : 32768u, &bar[buf]);
+            }
+        } else {
+            for (uint32_t i = threadIdx.x; i < len; i += blockDim.x) dst[i] = ldg(src + i);
+        }
+    };
+    __syncthreads();   // mbarriers initialised, bnd written
+    if (b0 < b1) stage(0, b0);
+    __syncthreads();   // a plain-copied first segment is visible
+    for (uint64_t b = b0; b < b1; ++b) {
+        const uint32_t cur = (uint32_t)((b - b0) & 1u);
+        // the other buffer was last read for segment b-1, before the barrier
+        if (b + 1 < b1) stage(cur ^ 1u, b + 1);
+        // buffer cur's ((b - b0) >> 1)-th fill (a plain-copied segment is the array's
+        // last, so no bulk fill of its buffer follows)
+        if (bulk_ok(b)) mbar_wait(&bar[cur], (uint32_t)(((b - b0) >> 1) & 1u));
+        const K* SK = SK0 + cur * S;
+        const uint64_t lo = b * S;
+        const uint32_t len = (uint32_t)((n - lo) < S ? (n - lo) : S);
+        const K smax = SK[len - 1];
+        const K lower = b ? ldg(p.a + lo - 1) : (K)0;
+        const bool first = b == 0, last = b == B - 1;
+        const uint64_t q0 = bnd[b - b0], q1 = bnd[b - b0 + 1];
+        // the segment's blocks of 32 queries, split evenly over the 32 warps
+        const uint32_t nblk = (uint32_t)((q1 - q0 + 31) / 32);
+        const uint32_t bw0 = (uint32_t)((uint64_t)nblk * warp / 32), bw1 = (uint32_t)((uint64_t)nblk * (warp + 1) / 32);
+        for (uint32_t bs = bw0; bs < bw1; bs += 31) {
+            const uint32_t nr = (bw1 - bs) < 31u ? (bw1 - bs) : 31u;   // blocks this round
+            // splitters: lane l <= nr takes the first query of block bs + l (lane nr:
+            // the block after the round) and finds its position by bisection
+            const uint64_t si = q0 + 32ull * (bs + lane);
+            const bool shas = lane <= nr && si < q1;
+            const K sx = shas ? ldg(p.q + si) : (K)0;
+            const uint32_t sc = shas ? smem_lower_bound(SK, 0u, len, sx) : len;
+            for (uint32_t j0 = 0; j0 < nr; j0 += kSegInFlight) {
+                K xs[kSegInFlight];   // kSegInFlight blocks of queries in flight
+#pragma unroll
+                for (uint32_t u = 0; u < kSegInFlight; ++u) {
+                    const uint64_t ir = q0 + 32ull * (bs + j0 + u) + lane;
+                    xs[u] = (j0 + u < nr && ir < q1) ? load_stream(p.q + ir, true, pol_stream) : (K)0;
+                }
+#pragma unroll
+                for (uint32_t u = 0; u < kSegInFlight; ++u) {
+                    const uint32_t j = j0 + u;
+                    if (j >= nr) break;                              // warp-uniform
+                    const uint64_t ir = q0 + 32ull * (bs + j) + lane;
+                    const K sj = __shfl_sync(0xFFFFFFFFu, sx, j), sj1 = __shfl_sync(0xFFFFFFFFu, sx, j + 1);
+                    const uint32_t cl = __shfl_sync(0xFFFFFFFFu, sc, j), ch1 = __shfl_sync(0xFFFFFFFFu, sc, j + 1);
+                    const bool has1 = q0 + 32ull * (bs + j + 1) < q1;   // the next block exists
+                    const bool valid = ir < q1;
+                    const K x = valid ? xs[u] : sj;
+                    const bool inseg = (first || x > lower) && (last || x <= smax);
+                    const bool inbr = inseg && x >= sj && (!has1 || x <= sj1);
+                    // the bracket [cl, ch1] (shared by the warp); lanes outside it take [0, len]
+                    const uint32_t c = smem_lower_bound(SK, inbr ? cl : 0u, inbr ? ch1 : len, x);
+                    uint64_t lb;
+                    bool hit;
+                    if (inseg) {
+                        lb = lo + c;
+                        hit = c < len && SK[c] == x;
+                    } else {
+                        // outside the segment's key range (an unordered batch): the whole array
+                        lb = lower_bound_global(p.a, n, x);
+                        hit = lb < n && ldg(p.a + lb) == x;
+                    }
+                    if (valid) {
+                        const uint64_t res = enc<OB>(lb, hit);
+                        if constexpr (OB == 8) store_stream((uint64_t*)p.out + ir, res, true, pol_stream);
+                        else store_stream((uint32_t*)p.out + ir, (uint32_t)res, true, pol_stream);
+                    }
+                }
+            }
+        }
+        __syncthreads();   // b+1 staged; every search of b is done with its buffer
     }
 }
 
@@ -736,24 +884,47 @@ k_unpart(const PartParams<K> p) {
 
 // ---------------------------------------------------------------- launchers
 
-static uint64_t seg_smem_bytes(uint64_t n, uint32_t grid, uint32_t kb, uint32_t nbuf = 1) {
+// two buffers of one segment's keys + the per-segment query ranges
+static uint64_t seg_smem_bytes(uint64_t n, uint32_t grid, uint32_t kb) {
     const uint64_t S = 1ull << kSegLog2;
     const uint64_t B = (n + S - 1) / S;
     const uint64_t nb = (B + grid - 1) / grid + 1;
-    return nbuf * S * (4 + kb) + nb * 8 + 16;
+    return 2 * S * kb + nb * 8 + 16;
 }
 constexpr uint64_t kSegSmemMax = 200u * 1024u;
 
 template <class K, int D, int OB>
 static cudaError_t go_seg(const SegParams<K>& p, Grid grid, cudaStream_t s, bool* uns) {
-    // two segment buffers when they fit (DB), else one
-    const bool db = seg_smem_bytes(p.n, grid.sm_count, (uint32_t)sizeof(K), 2) <= kSegSmemMax;
-    auto kern = db ? k_seg_sorted<K, D, OB, true> : k_seg_sorted<K, D, OB, false>;
+    auto kern = k_seg_sorted<K, D, OB>;
     const uint32_t threads = 1024;
     uint64_t g = 0;
     grid.sched_static = 1;
     grid.ctas_per_sm = 1;
-    const uint32_t smem = (uint32_t)seg_smem_bytes(p.n, grid.sm_count, (uint32_t)sizeof(K), db ? 2u : 1u);
+    const uint32_t smem = (uint32_t)seg_smem_bytes(p.n, grid.sm_count, (uint32_t)sizeof(K));
+    cudaError_t e = plan_grid((const void*)kern, threads, smem, grid, grid.sm_count, carveout_for(smem, threads), &g, uns);
+    if (e != cudaSuccess || *uns) return e;
+    kern<<<(unsigned)g, threads, smem, s>>>(p);
+    count_launch();
+    return cudaGetLastError();
+}
+
+static uint64_t seg_smem_bytes_eytz(uint64_t n, uint32_t grid, uint32_t kb, uint32_t nbuf = 1) {
+    const uint64_t S = 1ull << kSegLog2;
+    const uint64_t B = (n + S - 1) / S;
+    const uint64_t nb = (B + grid - 1) / grid + 1;
+    return nbuf * S * (4 + kb) + nb * 8 + 16;
+}
+
+template <class K, int D, int OB>
+static cudaError_t go_seg_eytz(const SegParams<K>& p, Grid grid, cudaStream_t s, bool* uns) {
+    // two segment buffers when they fit (DB), else one
+    const bool db = seg_smem_bytes_eytz(p.n, grid.sm_count, (uint32_t)sizeof(K), 2) <= kSegSmemMax;
+    auto kern = db ? k_seg_sorted_eytz<K, D, OB, true> : k_seg_sorted_eytz<K, D, OB, false>;
+    const uint32_t threads = 1024;
+    uint64_t g = 0;
+    grid.sched_static = 1;
+    grid.ctas_per_sm = 1;
+    const uint32_t smem = (uint32_t)seg_smem_bytes_eytz(p.n, grid.sm_count, (uint32_t)sizeof(K), db ? 2u : 1u);
     cudaError_t e = plan_grid((const void*)kern, threads, smem, grid, grid.sm_count, carveout_for(smem, threads), &g, uns);
     if (e != cudaSuccess || *uns) return e;
     kern<<<(unsigned)g, threads, smem, s>>>(p);
@@ -765,13 +936,27 @@ cudaError_t launch_seg_sorted(int kb, int ob, const void* a, uint64_t n, const v
                               uint32_t stream_hint, Grid grid, cudaStream_t s, bool* uns) {
     constexpr int D = kSegLog2;
     const uint64_t S = 1ull << D;
-    if (seg_smem_bytes(n, grid.sm_count, (uint32_t)kb) > kSegSmemMax) { *uns = true; return cudaSuccess; }
+    // bracketed bisection over the staged keys for u32 keys, and for u64 keys
+    // with many queries per key (m >= 32 n: a block of 32 queries brackets ~1
+    // key); otherwise the image-tree descent, whose fixed D levels of 32-bit
+    // probes cost less than a 64-bit bisection of a wide bracket (measured,
+    // DESIGN.md §6.9, profiles/r2s3/seg_kernel_ab.jsonl).  BS_SEG_KERNEL=
+    // eytz|bracket forces one (A/B).
+    bool bracket = kb == 4 || m >= 32 * n;
+    if (const char* v = getenv("BS_SEG_KERNEL")) bracket = strcmp(v, "bracket") == 0 ? true : strcmp(v, "eytz") == 0 ? false : bracket;
+    if (bracket ? seg_smem_bytes(n, grid.sm_count, (uint32_t)kb) > kSegSmemMax
+                : seg_smem_bytes_eytz(n, grid.sm_count, (uint32_t)kb) > kSegSmemMax) {
+        *uns = true;
+        return cudaSuccess;
+    }
     if (kb == 8) {
         SegParams<uint64_t> p{(const uint64_t*)a, n, (const uint64_t*)q, m, out, (uint32_t)ob, (n + S - 1) / S, stream_hint};
-        return ob == 8 ? go_seg<uint64_t, D, 8>(p, grid, s, uns) : go_seg<uint64_t, D, 4>(p, grid, s, uns);
+        if (bracket) return ob == 8 ? go_seg<uint64_t, D, 8>(p, grid, s, uns) : go_seg<uint64_t, D, 4>(p, grid, s, uns);
+        return ob == 8 ? go_seg_eytz<uint64_t, D, 8>(p, grid, s, uns) : go_seg_eytz<uint64_t, D, 4>(p, grid, s, uns);
     }
     SegParams<uint32_t> p{(const uint32_t*)a, n, (const uint32_t*)q, m, out, (uint32_t)ob, (n + S - 1) / S, stream_hint};
-    return ob == 8 ? go_seg<uint32_t, D, 8>(p, grid, s, uns) : go_seg<uint32_t, D, 4>(p, grid, s, uns);
+    if (bracket) return ob == 8 ? go_seg<uint32_t, D, 8>(p, grid, s, uns) : go_seg<uint32_t, D, 4>(p, grid, s, uns);
+    return ob == 8 ? go_seg_eytz<uint32_t, D, 8>(p, grid, s, uns) : go_seg_eytz<uint32_t, D, 4>(p, grid, s, uns);
 }
 
 // workspace layout of the GLOBAL mode (all offsets 256-B aligned)

@@ -24,6 +24,14 @@ def seg_run(idx, q, ob):
     return run(idx, q, ob, reorder=bs.REORDER_SORTED)
 
 
+@pytest.fixture(params=["eytz", "bracket"])
+def seg_kernel(request, monkeypatch):
+    """Both SORTED kernels (seg.cu picks by queries per key; BS_SEG_KERNEL forces
+    one): the image-tree descent and the bracketed bisection."""
+    monkeypatch.setenv("BS_SEG_KERNEL", request.param)
+    return request.param
+
+
 def queries_for(keys, m, seed, order):
     q = workload.gen_queries(keys, m, seed=seed, hit_ratio=0.7)
     adv = workload.adversarial_queries(keys[:: max(1, keys.size // 500)], seed=seed, extra=300)
@@ -33,7 +41,7 @@ def queries_for(keys, m, seed, order):
 
 @pytest.mark.parametrize("kb", [4, 8])
 @pytest.mark.parametrize("order", ["sorted", "random"])
-def test_seg_edge_sizes(kb, order):
+def test_seg_edge_sizes(kb, order, seg_kernel):
     for t, n in enumerate([1, 2, 3, 100, S - 1, S, S + 1, 2 * S, 3 * S + 5, 100003]):
         keys = workload.gen_keys(n, kb, seed=300 + t)
         q = queries_for(keys, 20000, 400 + t, order)
@@ -45,7 +53,7 @@ def test_seg_edge_sizes(kb, order):
 
 
 @pytest.mark.parametrize("kind", ["dups", "narrow", "clustered", "top"])
-def test_seg_key_distributions(kind):
+def test_seg_key_distributions(kind, seg_kernel):
     rng = np.random.default_rng({"dups": 1, "narrow": 2, "clustered": 3, "top": 4}[kind])
     n = 5 * S + 77
     if kind == "dups":
@@ -68,7 +76,7 @@ def test_seg_key_distributions(kind):
         idx.close()
 
 
-def test_seg_config3_sorted_sample():
+def test_seg_config3_sorted_sample(seg_kernel):
     """BASELINE configs[2] keys, pre-sorted 2^24-query batch: sampled oracle + every output's invariant."""
     import bench
     dk, dq, _ = bench._gen("config3", 0, 1, "strong", "sorted", "cuda")
