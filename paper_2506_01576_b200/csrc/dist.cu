@@ -50,13 +50,15 @@ struct DistState {
     void* d_recvq = nullptr;          // recv_cap keys
     uint64_t* d_recvres = nullptr;    // recv_cap results
     uint64_t* d_backres = nullptr;    // max_m results
+    void* d_ws = nullptr;             // workspace of the owner's out-of-place lookup (layout.reorder
+    uint64_t ws_bytes = 0;            // GLOBAL / BUCKET) for recv_cap queries; NULL: in-place lookup
 };
 
 void destroy_dist_state(Index* ix) {
     DistState* d = ix->dist;
     if (!d) return;
     void* bufs[] = {d->d_shard_max, d->d_dest, d->d_perm, d->d_counts, d->d_sendq, d->d_recvq, d->d_recvres,
-                    d->d_backres};
+                    d->d_backres, d->d_ws};
     for (void* b : bufs)
         if (b) cudaFree(b);
     delete d;
@@ -265,6 +267,20 @@ int bs_build_dist(void* comm, const void* local_keys, uint64_t n_local, int mode
         e = cudaMalloc(a.p, a.b);
         if (e != cudaSuccess) return cleanup(fail_cuda(e, "cudaMalloc(exchange buffers)"));
     }
+    // the owner's lookup of the received queries in the layout's out-of-place
+    // mode (the same local lookup as the fused peer path): its workspace, sized
+    // for the receive capacity; a layout / size the mode cannot take keeps the
+    // in-place lookup
+    const uint32_t ro = ix->layout.reorder;
+    if (ro == BS_REORDER_GLOBAL || ro == BS_REORDER_BUCKET) {
+        uint64_t wb = 0;
+        if (bs_workspace_bytes(ix, R, nullptr, &wb) == BS_OK && wb) {
+            e = cudaMalloc(&d->d_ws, wb);
+            if (e != cudaSuccess) return cleanup(fail(BS_ERR_OOM, "bs_build_dist: cudaMalloc(%llu B lookup workspace)",
+                                                      (unsigned long long)wb));
+            d->ws_bytes = wb;
+        }
+    }
     return BS_OK;
 }
 
@@ -343,8 +359,13 @@ int bs_lookup_dist(const void* idx, const void* local_queries, uint64_t m_local,
     if (racc) {
         bs_launch Ld;
         bs_launch_default(idx, &Ld);
-        if (Ld.reorder == BS_REORDER_GLOBAL || Ld.reorder == BS_REORDER_BUCKET) Ld.reorder = BS_REORDER_NONE;   // no workspace here
-        int rc = bs_lookup_ex(idx, d->d_recvq, racc, d->d_recvres, s, &Ld);
+        int rc;
+        if (d->d_ws) {
+            rc = bs_lookup_ws(idx, d->d_recvq, racc, d->d_recvres, s, &Ld, d->d_ws, d->ws_bytes);
+        } else {
+            if (Ld.reorder == BS_REORDER_GLOBAL || Ld.reorder == BS_REORDER_BUCKET) Ld.reorder = BS_REORDER_NONE;
+            rc = bs_lookup_ex(idx, d->d_recvq, racc, d->d_recvres, s, &Ld);
+        }
         if (rc != BS_OK) return rc;
         k_add_base<<<grid_of(racc), 256, 0, s>>>(d->d_recvres, racc, d->base[me]);
         count_launch();

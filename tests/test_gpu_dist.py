@@ -46,3 +46,20 @@ def test_dist_overflow_rejected(comm):
     out = torch.empty(11, dtype=torch.int64, device="cuda")
     with pytest.raises(bs.BsError):
         bs.bs_lookup_dist(idx, q, 11, out)
+
+
+@pytest.mark.parametrize("reorder,n", [(5, 100003), (5, 3 << 20), (4, 100003)])
+def test_dist_partitioned_out_of_place_lookup(comm, reorder, n):
+    """layout.reorder = BUCKET / GLOBAL: bs_build_dist allocates the workspace for
+    its receive capacity and the owner looks the received queries up in that
+    mode (as the fused peer path does); several calls reuse it."""
+    keys = workload.gen_keys(n, 8, seed=13)
+    lay = bs.bs_layout_default(key_bytes=8, out_bytes=8, variant=bs.KARY, reorder=reorder)
+    idx = bs.bs_build_dist(comm, P.as_torch(keys), keys.size, bs.DIST_PARTITIONED, lay, 200000)
+    out = torch.empty(200000, dtype=torch.int64, device="cuda")
+    for call, m in enumerate((200000, 8193, 1)):
+        q = workload.gen_queries(keys, m, seed=14 + call, hit_ratio=0.6)
+        bs.bs_lookup_dist(idx, P.as_torch(q), m, out)
+        torch.cuda.synchronize()
+        assert np.array_equal(P.to_numpy_unsigned(out[:m], 8), oracle.lookup(keys, q)), f"call {call}"
+    idx.close()
