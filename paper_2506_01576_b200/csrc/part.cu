@@ -526,6 +526,30 @@ k_bk_scan(uint32_t* __restrict__ cnt, uint32_t* __restrict__ tot, uint32_t G, ui
     }
 }
 
+// a query and its (bucket, slot) word side by side in the sorted tile: one
+// 16-B (u64) / 8-B (u32) shared store and load per query instead of two each
+template <class K> struct BkPair;
+template <> struct alignas(16) BkPair<uint64_t> { uint64_t k; uint32_t bp, pad; };
+template <> struct alignas(8) BkPair<uint32_t> { uint32_t k; uint32_t bp; };
+
+template <class K>
+__device__ __forceinline__ void st_pair(BkPair<K>* d, K k, uint32_t bp) {
+    if constexpr (sizeof(K) == 8) *reinterpret_cast<uint4*>(d) = make_uint4((uint32_t)k, (uint32_t)(k >> 32), bp, 0u);
+    else *reinterpret_cast<uint2*>(d) = make_uint2((uint32_t)k, bp);
+}
+template <class K>
+__device__ __forceinline__ void ld_pair_smem(const BkPair<K>* s, K& k, uint32_t& bp) {
+    if constexpr (sizeof(K) == 8) {
+        const uint4 v = *reinterpret_cast<const uint4*>(s);
+        k = ((uint64_t)v.y << 32) | v.x;
+        bp = v.z;
+    } else {
+        const uint2 v = *reinterpret_cast<const uint2*>(s);
+        k = v.x;
+        bp = v.y;
+    }
+}
+
 // ---- pass 3: partition (tile t on CTA t % G, as in k_bk_hist)
 //
 // Thread i owns buckets [i BPT, (i+1) BPT) (BPT = kBkFineMax / threads = 1): their
@@ -540,9 +564,8 @@ k_bk_part(const BkParams<K> p) {
     constexpr uint32_t NW = kBkPThreads / 32;
     extern __shared__ __align__(16) uint32_t sm[];
     const uint32_t B = p.B;
-    K* stq = reinterpret_cast<K*>(sm);                        // [T] queries, bucket order
-    uint32_t* sbp = reinterpret_cast<uint32_t*>(stq + T);     // [T] bucket | original slot << 16, bucket order
-    uint32_t* hist = sbp + T;                                 // [kBkFineMax] tile counts (ranks by atomics)
+    BkPair<K>* st = reinterpret_cast<BkPair<K>*>(sm);         // [T] query + (bucket | original slot << 16), bucket order
+    uint32_t* hist = reinterpret_cast<uint32_t*>(st + T);     // [kBkFineMax] tile counts (ranks by atomics)
     uint32_t* loff = hist + kBkFineMax;                       // [kBkFineMax] tile run starts (sorted order)
     uint32_t* rbase = loff + kBkFineMax;                      // [kBkFineMax] global position of run b minus its sorted start
     uint32_t* wsum = rbase + kBkFineMax;                      // [NW] warp totals
@@ -662,26 +685,18 @@ k_bk_part(const BkParams<K> p) {
             if (br[e] == 0xFFFFu) continue;
             const uint32_t b = br[e] & 0xFFFFu;
             const uint32_t sidx = loff[b] + (br[e] >> 16);
-            stq[sidx] = x[e];
-            sbp[sidx] = b | ((e * kBkPThreads + threadIdx.x) << 16);
+            st_pair<K>(st + sidx, x[e], b | ((e * kBkPThreads + threadIdx.x) << 16));
         }
         __syncthreads();   // (5) the sorted tile
         // each run to its place in its bucket's region (consecutive within a run;
         // evict_normal: the run's partial lines are completed by this CTA's next
         // tile and must stay in L2 until then), and the tile's (bucket, slot) list
         for (uint32_t sidx = threadIdx.x; sidx < cntq; sidx += blockDim.x) {
-            const uint32_t w = sbp[sidx];
-            store_stream(p.rq + (uint32_t)(rbase[w & 0xFFFFu] + sidx), stq[sidx], true, pol_run);
-        }
-        // the (bucket, slot) list: 16-B vector stores (fewer store instructions in flight)
-        if (cntq == T) {
-            for (uint32_t j4 = threadIdx.x * 4; j4 < T; j4 += blockDim.x * 4) {
-                const uint4 w4 = *reinterpret_cast<const uint4*>(sbp + j4);
-                asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;"
-                             :: "l"(p.bp + b0 + j4), "r"(w4.x), "r"(w4.y), "r"(w4.z), "r"(w4.w), "l"(pol) : "memory");
-            }
-        } else {
-            for (uint32_t sidx = threadIdx.x; sidx < cntq; sidx += blockDim.x) store_stream(p.bp + b0 + sidx, sbp[sidx], true, pol);
+            K k;
+            uint32_t w;
+            ld_pair_smem<K>(st + sidx, k, w);
+            store_stream(p.rq + (uint32_t)(rbase[w & 0xFFFFu] + sidx), k, true, pol_run);
+            store_stream(p.bp + b0 + sidx, w, true, pol);
         }
     }
 }
@@ -1066,7 +1081,7 @@ static cudaError_t go_bucket(BkParams<K> p, const BkLayout& L, char* ws, cudaStr
         k_bk_scan<<<(B + 31) / 32, 1024, 0, s>>>(p.cnt, p.tot, p.Gp, B);
         count_launch();
         {
-            const uint32_t smem = kBkTile * ((uint32_t)sizeof(K) + 4u) + 4u * (3u * kBkFineMax + 32u);
+            const uint32_t smem = kBkTile * (uint32_t)sizeof(BkPair<K>) + 4u * (3u * kBkFineMax + 32u);
             e = bk_launch(pm ? (const void*)k_bk_part<K, true> : (const void*)k_bk_part<K, false>, kBkPThreads, smem, p.Gp, &p, s);
             if (e != cudaSuccess) return e;
         }
