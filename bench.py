@@ -444,7 +444,7 @@ def main():
     ap.add_argument("--nreg", type=int, default=0)
     ap.add_argument("--reorder", type=int, default=-1,
                     help="bs_reorder; -1 = the config's fastest mode: BUCKET (5) for a random batch over an "
-                         "array larger than L2 (configs 3-4), SORTED (3) for a pre-sorted batch, else NONE")
+                         "array larger than L2 (configs 3-5; config 5: the owner's lookup of its receive window), SORTED (3) for a pre-sorted batch, else NONE")
     ap.add_argument("--schedule", type=int, default=1)
     ap.add_argument("--hints", type=int, default=0x100, help="cache_hints bits; 256 = BS_HINT_AUTO (resolved at build)")
     ap.add_argument("--kary-mode", type=int, default=8,
