@@ -15,7 +15,7 @@
 //   k_bk_scan    per bucket: exclusive prefix of the CTA histograms
 //   k_bk_part    per tile of T = 8192 queries: rank each query in its bucket's
 //                run (shared atomic), counting-sort the tile by bucket in shared
-//                memory, append each run to the CTA's slice of its bucket's
+//                memory (query and slot word in one 16-B entry), append each run to the CTA's slice of its bucket's
 //                region (bucket-major, exact offsets: no global atomics, no
 //                overflow), and record for every sorted position its bucket and
 //                original slot
@@ -30,9 +30,14 @@
 //                order in shared memory, one coalesced store (Listing 2 l.35-39's
 //                "unsort", at batch scale)
 //
+// Peer window (bs_lookup_peer with layout.reorder = BUCKET, peer.cu): the same
+// passes over the receive window, the batch size read from the receive cursor
+// on the device (the PM kernel variants), and k_bk_unpart storing every result
+// into its source rank's return window instead of `out`.
+//
 // Bucket b covers the array positions [b*NB, (b+1)*NB): fine buckets hold 2^D
 // leaves of 32 B (NB = 2^17 u64 / 2^18 u32 keys), two-level buckets 2^D units of
-// 8 leaves of 64 B (16 MB of keys).  A query belongs to bucket #(bucket maxima <
+// 16 leaves of 32 B (16 MB of keys; 8 leaves of 64 B with BS_BUCKET_G8=1).  A query belongs to bucket #(bucket maxima <
 // q) (the last bucket also takes the queries above every key).  The bucket is
 // exact, so the per-bucket search never leaves its bucket.  DESIGN.md §6.11.
 #include <cstdlib>
