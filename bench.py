@@ -502,7 +502,12 @@ def main():
     stream = torch.cuda.Stream()
     dist_ms = None
     if mode == "partitioned":
-        idx = bs.bs_build_peer(dk, n_loc, lay, rank, world, m)
+        # each rank's batch holds m / world queries drawn from every shard (the
+        # untimed exchange in _gen), so each rank receives ~m: a receive window
+        # of m + 1/16 (an overflow would be flagged and fail the parity check)
+        # instead of the never-overflowing world * m keeps the window and the
+        # BUCKET workspace at ~18 GB per GPU at world 8 instead of ~73
+        idx = bs.bs_build_peer(dk, n_loc, lay, rank, world, m, recv_capacity=m + m // 16 + 8192)
         if world > 1:
             bs.bs_peer_connect_group(idx)
         else:
