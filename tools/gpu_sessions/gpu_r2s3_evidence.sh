@@ -12,6 +12,7 @@ B() { local name=$1; shift; timeout 900 python bench.py "$@" > $O/bench_$name.js
 B config3_kary --reorder 0 --no-e2e
 B config3_sorted --order sorted --no-e2e --no-naive
 B config3_global --reorder 4 --no-e2e --no-naive
+B config2_sorted --config config2 --order sorted --no-e2e --no-naive
 B config2 --config config2
 B config1 --config config1 --no-e2e
 B config4 --config config4 --steps 5
