@@ -285,9 +285,7 @@ __device__ __forceinline__ uint64_t bk_m(const BkParams<K>& p) {
 // it; a bin with more maxima continues by bisection, and maxima whose image
 // ties x's are compared exactly (galloping over the real maxima a[(j+1) NB - 1]).
 template <class K>
-__device__ __forceinline__ uint32_t bk_bucket(const BkParams<K>& p, const uint32_t* MS, const uint32_t* DIR, K x) {
-    const uint32_t fx = bk_img((uint64_t)x, p.gbase, p.gsh);
-    const uint32_t w = DIR[fx >> (32 - kBkBinsLog2)];
+__device__ __forceinline__ uint32_t bk_bucket_w(const BkParams<K>& p, const uint32_t* MS, uint32_t w, uint32_t fx, K x) {
     uint32_t l = w & 0xFFFFu, h = w >> 16;
     bool more = false, tie = false;
     if (l < h) {
@@ -330,13 +328,16 @@ __device__ __forceinline__ uint32_t bk_bucket(const BkParams<K>& p, const uint32
 // The common case of bk_bucket without branches: the bin's first candidate
 // maximum decides unless the bin holds another maximum below x or an image
 // ties x's; *rare is set for those, which the caller re-resolves with bk_bucket.
+// D2[bin] = (lo | hi << 16, MS[lo]): the bin's candidate range and its first
+// maximum in one 8-B shared load (one random shared access per query, not two)
 template <class K>
-__device__ __forceinline__ uint32_t bk_bucket_fast(const BkParams<K>& p, const uint32_t* MS, const uint32_t* DIR,
-                                                   K x, bool& rare) {
-    const uint32_t fx = bk_img((uint64_t)x, p.gbase, p.gsh);
-    const uint32_t w = DIR[fx >> (32 - kBkBinsLog2)];
+__device__ __forceinline__ uint32_t bk_bucket_fast(const BkParams<K>& p, const uint2* D2, K x, uint32_t& fx,
+                                                   uint32_t& w, bool& rare) {
+    fx = bk_img((uint64_t)x, p.gbase, p.gsh);
+    const uint2 d = D2[fx >> (32 - kBkBinsLog2)];
+    w = d.x;
     const uint32_t l = w & 0xFFFFu, h = w >> 16;
-    const uint32_t v = MS[l];   // l <= B - 1: always a maximum
+    const uint32_t v = d.y;   // MS[l]: l <= B - 1 is always a maximum
     const bool has = l < h;
     const bool lt = has && v < fx;
     rare = (lt && l + 1 < h) || (has && v == fx);
@@ -345,9 +346,12 @@ __device__ __forceinline__ uint32_t bk_bucket_fast(const BkParams<K>& p, const u
 
 // stage the bucket maxima images and the packed directory (plain loads; once per CTA)
 template <class K>
-__device__ __forceinline__ void bk_stage_dir(const BkParams<K>& p, uint32_t* MS, uint32_t* DIR) {
+__device__ __forceinline__ void bk_stage_dir2(const BkParams<K>& p, uint32_t* MS, uint2* D2) {
     for (uint32_t i = threadIdx.x; i < p.B; i += blockDim.x) MS[i] = p.mx[i];
-    for (uint32_t i = threadIdx.x; i < kBkBins; i += blockDim.x) DIR[i] = (uint32_t)p.dir[i] | ((uint32_t)p.dir[i + 1] << 16);
+    for (uint32_t i = threadIdx.x; i < kBkBins; i += blockDim.x) {
+        const uint32_t lo = p.dir[i];
+        D2[i] = make_uint2(lo | ((uint32_t)p.dir[i + 1] << 16), ldg(p.mx + lo));
+    }
 }
 
 // block-wide exclusive scan of v[0..N) in place (blockDim.x = 1024); returns the total
@@ -419,8 +423,8 @@ k_bk_hist(const BkParams<K> p) {
     const uint32_t B4 = (p.B + 3u) & ~3u;
     uint32_t* MS = sm;
     uint32_t* hist = MS + B4;
-    uint32_t* DIR = hist + B4;                                // [kBkBins]
-    bk_stage_dir(p, MS, DIR);
+    uint2* D2 = reinterpret_cast<uint2*>(hist + B4);          // [kBkBins] (lo | hi << 16, MS[lo])
+    bk_stage_dir2(p, MS, D2);
     for (uint32_t b = threadIdx.x; b < p.B; b += blockDim.x) hist[b] = 0;
     __syncthreads();
     const uint64_t pol = p.stream_hint ? policy_evict_first() : policy_evict_normal();
@@ -464,11 +468,12 @@ k_bk_hist(const BkParams<K> p) {
             for (uint32_t e = 0; e < E2; ++e) {
                 const uint32_t j = 2 * (e * kBkPThreads + threadIdx.x);
                 bool r0, r1;
-                uint32_t b0v = bk_bucket_fast(p, MS, DIR, x[2 * e], r0);
-                uint32_t b1v = bk_bucket_fast(p, MS, DIR, x[2 * e + 1], r1);
+                uint32_t f0, f1, w0, w1;
+                uint32_t b0v = bk_bucket_fast(p, D2, x[2 * e], f0, w0, r0);
+                uint32_t b1v = bk_bucket_fast(p, D2, x[2 * e + 1], f1, w1, r1);
                 if (__builtin_expect(r0 || r1, 0)) {
-                    b0v = bk_bucket(p, MS, DIR, x[2 * e]);
-                    b1v = bk_bucket(p, MS, DIR, x[2 * e + 1]);
+                    b0v = bk_bucket_w(p, MS, w0, f0, x[2 * e]);
+                    b1v = bk_bucket_w(p, MS, w1, f1, x[2 * e + 1]);
                 }
                 atomicAdd(&hist[b0v], 1u);
                 atomicAdd(&hist[b1v], 1u);
@@ -484,7 +489,8 @@ k_bk_hist(const BkParams<K> p) {
 #pragma unroll
             for (uint32_t h = 0; h < 2; ++h) {
                 if (j + h < cntq) {
-                    const uint32_t b = bk_bucket(p, MS, DIR, x[2 * e + h]);
+                    const uint32_t fx = bk_img((uint64_t)x[2 * e + h], p.gbase, p.gsh);
+                    const uint32_t b = bk_bucket_w(p, MS, D2[fx >> (32 - kBkBinsLog2)].x, fx, x[2 * e + h]);
                     atomicAdd(&hist[b], 1u);
                     b01 |= b << (16 * h);
                 }
@@ -1079,7 +1085,7 @@ static cudaError_t go_bucket(BkParams<K> p, const BkLayout& L, char* ws, cudaStr
     cudaError_t e;
     if (phase != 2) {
         {
-            const uint32_t smem = 8u * B4 + 4u * kBkBins;
+            const uint32_t smem = 8u * B4 + 8u * kBkBins;
             e = bk_launch(pm ? (const void*)k_bk_hist<K, true> : (const void*)k_bk_hist<K, false>, kBkPThreads, smem, p.Gp, &p, s);
             if (e != cudaSuccess) return e;
         }
