@@ -142,6 +142,35 @@ def test_bucket_config3_sample():
     idx.close()
 
 
+@pytest.mark.timeout(900)
+def test_bucket_max_batch():
+    """The largest batch BUCKET mode takes (m < 2^32, ragged: 2^32 - 2^20 - 3
+    u32 queries over 2^26 u32 keys, 256 fine buckets): bucket counts, run
+    positions and the search's item ranges are 32-bit and wrap nowhere.  Checked
+    on 2^16 sampled outputs and on the first and last 2^16 outputs."""
+    import workload.device as wd
+    free, _ = torch.cuda.mem_get_info()
+    m = (1 << 32) - (1 << 20) - 3
+    if free < 100 * (1 << 30):
+        pytest.skip("needs ~100 GB of free device memory")
+    dk = wd.gen_keys(1 << 26, 4, device="cuda")
+    dq = wd.gen_queries(dk, m, hit_ratio=0.7)
+    out = torch.empty(m, dtype=torch.int32, device="cuda")
+    idx = bs.bs_build(dk, dk.numel(), bs.bs_layout_default(key_bytes=4, out_bytes=4))
+    nb = bs.bs_workspace_bytes(idx, m, reorder=bs.REORDER_BUCKET)
+    ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    bs.bs_lookup_ws(idx, dq, m, out, None, ws, nb, reorder=bs.REORDER_BUCKET)
+    torch.cuda.synchronize()
+    kh = P.to_numpy_unsigned(dk, 4)
+    samp = np.concatenate([np.arange(1 << 16), np.arange(m - (1 << 16), m),
+                           np.random.default_rng(9).integers(0, m, size=1 << 16)])
+    st = torch.from_numpy(samp).cuda()
+    got = P.to_numpy_unsigned(out[st], 4)
+    want = oracle.lookup(kh, P.to_numpy_unsigned(dq[st], 4), out_bytes=4)
+    assert np.array_equal(got, want), f"first mismatch at {samp[np.flatnonzero(got != want)[:5]]}"
+    idx.close()
+
+
 # ------------------------------------------------------------------ two-level buckets (large arrays)
 
 @pytest.mark.parametrize("kb", [4, 8])
