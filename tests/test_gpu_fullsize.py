@@ -124,3 +124,34 @@ def test_fullsize_bucket(cfg):
     idx.close()
     del dk, dq, out, ws
     torch.cuda.empty_cache()
+
+
+@pytest.mark.timeout(900)
+@pytest.mark.parametrize("reorder", [0, 3])
+def test_batch_beyond_2_32(reorder):
+    """m = 2^32 + 5 u32 queries through the K-ary kernel (reorder 0) and the
+    SORTED kernels (reorder 3, a sorted batch): 64-bit query offsets
+    everywhere.  Checked on the first / last 2^16 outputs and 2^16 sampled."""
+    import workload.device as wd
+    free, _ = torch.cuda.mem_get_info()
+    if free < 60 * (1 << 30):
+        pytest.skip("needs ~60 GB of free device memory")
+    m = (1 << 32) + 5
+    dk = wd.gen_keys(1 << 24, 4, device="cuda")
+    if reorder == 3:
+        # an ordered batch without a device sort (torch sorts at most INT_MAX
+        # elements): every key 256 times, then 5 copies of the largest
+        dq = torch.cat([dk.repeat_interleave(256), dk[-1:].expand(5)]).contiguous()
+    else:
+        dq = wd.gen_queries(dk, m, hit_ratio=0.5)
+    out = torch.empty(m, dtype=torch.int32, device="cuda")
+    idx = bs.bs_build(dk, dk.numel(), bs.bs_layout_default(key_bytes=4, out_bytes=4))
+    bs.bs_lookup_ex(idx, dq, m, out, None, reorder=reorder)
+    torch.cuda.synchronize()
+    samp = np.concatenate([np.arange(1 << 16), np.arange(m - (1 << 16), m),
+                           np.random.default_rng(11).integers(0, m, size=1 << 16)])
+    st = torch.from_numpy(samp).cuda()
+    got = P.to_numpy_unsigned(out[st], 4)
+    want = oracle.lookup(P.to_numpy_unsigned(dk, 4), P.to_numpy_unsigned(dq[st], 4), out_bytes=4)
+    assert np.array_equal(got, want), f"first mismatch at {samp[np.flatnonzero(got != want)[:5]]}"
+    idx.close()
