@@ -155,3 +155,35 @@ def test_batch_beyond_2_32(reorder):
     want = oracle.lookup(P.to_numpy_unsigned(dk, 4), P.to_numpy_unsigned(dq[st], 4), out_bytes=4)
     assert np.array_equal(got, want), f"first mismatch at {samp[np.flatnonzero(got != want)[:5]]}"
     idx.close()
+
+
+@pytest.mark.timeout(900)
+def test_bucket_max_keys():
+    """BUCKET mode at the largest array it takes: 2^31 u64 keys = 1024 two-level
+    buckets of 16 MB (kBkMaxBuckets), 2^26 queries (hits, misses between keys,
+    below / above every key).  Keys are built strictly increasing without a
+    device sort (torch sorts at most INT_MAX elements): key i = i * 2^32 + a
+    16-bit hash of i.  Checked against the oracle on 2^16 sampled outputs."""
+    free, _ = torch.cuda.mem_get_info()
+    if free < 40 * (1 << 30):
+        pytest.skip("needs ~40 GB of free device memory")
+    n, m = 1 << 31, 1 << 26
+    i = torch.arange(n, dtype=torch.int64, device="cuda")
+    dk = (i << 32) | ((i * 0x9E3779B1) >> 7 & 0xFFFF)
+    del i
+    g = torch.Generator(device="cuda").manual_seed(5)
+    pick = torch.randint(0, n, (m,), device="cuda", generator=g)
+    dq = dk[pick] + (torch.randint(0, 2, (m,), device="cuda", generator=g) << 16)   # every other one a miss
+    dq[:3] = torch.tensor([0, 1 << 62, -1], dtype=torch.int64, device="cuda")      # below / inside / above
+    out = torch.empty(m, dtype=torch.int64, device="cuda")
+    idx = bs.bs_build(dk, n, bs.bs_layout_default(input_sorted=1))
+    nb = bs.bs_workspace_bytes(idx, m, reorder=bs.REORDER_BUCKET)
+    ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    bs.bs_lookup_ws(idx, dq, m, out, None, ws, nb, reorder=bs.REORDER_BUCKET)
+    torch.cuda.synchronize()
+    samp = np.concatenate([np.arange(3), np.random.default_rng(13).integers(0, m, size=1 << 16)])
+    st = torch.from_numpy(samp).cuda()
+    got = P.to_numpy_unsigned(out[st], 8)
+    want = oracle.lookup(P.to_numpy_unsigned(dk, 8), P.to_numpy_unsigned(dq[st], 8), out_bytes=8)
+    assert np.array_equal(got, want), f"first mismatch at {samp[np.flatnonzero(got != want)[:5]]}"
+    idx.close()
