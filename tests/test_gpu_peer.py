@@ -54,7 +54,7 @@ def test_peer_world1(kb):
     idx.close()
 
 
-@pytest.mark.parametrize("kb,n", [(8, 200003), (4, 200003), (8, 3 << 20), (4, 5 << 20)])
+@pytest.mark.parametrize("kb,n", [(8, 1), (4, 7), (8, 200003), (4, 200003), (8, 3 << 20), (4, 5 << 20)])
 def test_peer_world1_bucket(kb, n):
     """layout.reorder = BUCKET: the window is partitioned and searched by the
     bucket pipeline (part.cu), whose unpartition stores every result into its
